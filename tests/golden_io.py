@@ -1,0 +1,46 @@
+"""Helpers to read the committed golden fixtures (tests/golden/*.npz).
+
+The fixtures were written by ``tests/golden/make_golden.py`` from the reference
+package itself; nothing here touches ``/root/reference`` at run time.
+"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+
+GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+
+
+def load(name: str):
+    return np.load(os.path.join(GOLDEN, f"{name}.npz"), allow_pickle=False)
+
+
+def graph_layers(z):
+    return [(z[f"nbrs{l}"], z[f"cnts{l}"]) for l in range(int(z["n_layers"]))]
+
+
+def model_layers(z, prefix=""):
+    n = int(z[f"{prefix}n_mlp"])
+    return [(z[f"{prefix}W{m}"], z[f"{prefix}b{m}"]) for m in range(n)], z[f"{prefix}A"], \
+        bool(z[f"{prefix}relu"])
+
+
+def param_sets(z):
+    out = []
+    i = 0
+    while f"p{i}/params" in z.files:
+        k, kp, hops, ef = (int(v) for v in z[f"p{i}/params"])
+        out.append((i, dict(k=k, k_parallel=kp, hops=hops, ef=ef)))
+        i += 1
+    return out
+
+
+def expected(z, pi):
+    p = f"p{pi}/"
+    return {key: z[p + "res_" + key] for key in
+            ("ids", "scores", "n", "evals", "visited", "best_hop", "per_layer")}
+
+
+SEARCH_FIXTURES = ["search_d64_z2", "search_d128_z3", "search_d32_shuffled"]
