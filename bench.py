@@ -1,0 +1,377 @@
+"""Benchmark: queries/sec at recall@100 of the B200 HiPANNS hot path (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {gmpgr,reference}]
+                    [--config cfg3|cfg2|cfg1|small]
+
+Workload (default cfg3 = BASELINE configs[2], the config the metric is quoted on):
+10M items, 128-d embeddings, degree-48 graph (m=24), 3-relation MLP (64, 64),
+top-100, SearchParams(k=100, k_parallel=8, hops=3, ef=200) (reference defaults,
+evalharness.py:84-87), a 65,536-query batch per GPU (weak scaling: every rank holds a
+replica of the index and searches its own query batch; no data-path collective).
+
+A step = one batched C-HiPANNS over the per-GPU query batch = ONE launch of
+hipanns_search_kernel (exact-fp32 scoring fused).  `value` uses device-resident
+inputs, CUDA events on the launching stream, max over ranks.  `e2e` goes through the
+public host API (host buffers, H2D of users + D2H of ids/scores/stats inside the
+timed region).  `--impl reference` times the reference algorithm's CPU restatement
+(oracle/c, all host threads) on a bounded query sample of the same workload.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+PARAMS = dict(k=100, k_parallel=8, hops=3, ef=200)
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "_fallback": True}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.out = ""
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.out, _ = self.proc.communicate(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = [r.split(",") for r in (self.out or "").strip().splitlines() if r.count(",") >= 8]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[1]) for r in rows]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].strip() == "Active"})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(rows[0][2]),
+                "reasons": reasons, "samples": len(rows)}
+
+
+def algorithmic_bytes(evals, rows, nbrs, d_h, k, bytes_per_elem=4):
+    """B_q = 4*NbrIds + 4*Rows + s_e*d_h*E + 8k, summed over queries."""
+    return float(4 * nbrs.sum() + 4 * rows.sum() + bytes_per_elem * d_h * evals.sum()
+                 + 8 * k * len(evals))
+
+
+def flops_per_eval(model):
+    dims = [l[0].shape[0] for l in model.metric.layers]
+    d_h = model.d_h
+    z = dims[-1]
+    f = d_h * dims[0]  # item half of layer 0 (user half hoisted per query)
+    prev = dims[0]
+    for o in dims[1:]:
+        f += prev * o
+        prev = o
+    return 2 * (f + z)
+
+
+def dist_setup(n_gpus):
+    import torch
+
+    if n_gpus > 1 or int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        import torch.distributed as dist
+
+        rank = int(os.environ.get("RANK", "0"))
+        local = int(os.environ.get("LOCAL_RANK", str(rank)))
+        torch.cuda.set_device(local)
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        return dist, rank, dist.get_world_size(), local
+    torch.cuda.set_device(0)
+    return None, 0, 1, 0
+
+
+def cpu_search(wl, queries, nthreads=None):
+    """The reference algorithm's C restatement (oracle/c) on the host cores."""
+    from oracle import oracle_c
+
+    ids, levels, layers, entry = wl.index.graph_view()
+    m = wl.model.metric
+    t0 = time.perf_counter()
+    r = oracle_c.search(layers, entry, ids, m.layers, m.attention, m.activation == "relu",
+                        wl.items_host, queries, **PARAMS, nthreads=nthreads)
+    return r, time.perf_counter() - t0
+
+
+def cpu_probe(wl, threads):
+    """Throughput probe (2 rounds, the first absorbs per-thread visited-array setup)."""
+    probe = wl.users[: max(64, 8 * threads)]
+    cpu_search(wl, probe[: 2 * threads], threads)
+    _, t = cpu_search(wl, probe, threads)
+    return len(probe) / t
+
+
+def cpu_baseline(wl, target_s=15.0):
+    from oracle import oracle_c
+
+    threads = oracle_c.lib().oracle_num_threads()
+    qps = cpu_probe(wl, threads)
+    n = int(min(len(wl.users), max(64, qps * target_s)))
+    r, t = cpu_search(wl, wl.users[:n], threads)
+    return r, n, t, threads
+
+
+def run_reference(args):
+    dist, rank, world, local = dist_setup(args.gpus)
+    if rank != 0:
+        return 0
+    from paper_2502_11490_b200 import workload
+
+    wl = workload.make(args.config, rank=0, device=local, host_items=True)
+    log(f"[reference] workload {args.config} built in {wl.build_s:.1f}s")
+    from oracle import oracle_c
+
+    threads = oracle_c.lib().oracle_num_threads()
+    qps = cpu_probe(wl, threads)
+    per_step = int(min(len(wl.users), max(64, qps * args.ref_step_s)))
+    for w in range(args.warmup):
+        cpu_search(wl, wl.users[:per_step], threads)
+    t_tot = 0.0
+    for s in range(args.steps):
+        lo = (s * per_step) % max(1, len(wl.users) - per_step + 1)
+        _, t = cpu_search(wl, wl.users[lo:lo + per_step], threads)
+        t_tot += t
+    qps = per_step * args.steps / t_tot
+    line = {
+        "impl": "reference", "metric": "queries/sec at recall@100", "value": qps,
+        "unit": "queries/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * t_tot / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_of(args, wl),
+        "cpu_baseline": {"value": qps, "unit": "queries/s", "cores": threads, "kind": "port",
+                         "sample": f"{per_step} queries per step of the {args.config} batch, "
+                                   f"oracle/c (C restatement of nann.c_hipanns + einsum-order "
+                                   f"relevance), {threads} OpenMP threads"},
+        "e2e": {"value": qps, "unit": "queries/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+        "gpu_launches": 0,
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def config_of(args, wl):
+    N, d = wl.index._n, wl.model.d_h
+    return {"workload": f"{args.config}: {N} items, {d}-d, degree-{2 * wl.index.m} graph "
+                        f"(m={wl.index.m}), Z={wl.model.z_dim} MLP(64,64), top-100, "
+                        f"{len(wl.users)} queries per GPU",
+            "params": dict(PARAMS), "n_items": N, "d_h": d, "queries_per_gpu": len(wl.users),
+            "parallelism": f"query-parallel replicas x{args.gpus}",
+            "l2": "inputs larger than L2 (graph + embeddings >> 126 MB)",
+            "graph": "GPU producer (builder.py): reference level draws + symmetric pruned k-NN"}
+
+
+def run_gmpgr(args):
+    import torch
+
+    dist, rank, world, local = dist_setup(args.gpus)
+    from paper_2502_11490_b200 import _lib, workload
+    from paper_2502_11490_b200.search import SearchParams, c_hipanns_batch, brute_force_batch
+
+    dev = local
+    want_cpu = (world == 1 and not args.no_cpu_baseline)
+    wl = workload.make(args.config, rank=rank, device=dev, host_items=want_cpu)
+    log(f"[rank {rank}] workload {args.config} built in {wl.build_s:.1f}s, "
+        f"layers {wl.index.layer_node_counts()}")
+    model, index = wl.model, wl.index
+    metric = model.metric
+    dm = metric.device_model(dev)
+    g = index.device_graph(dev)
+    it = _lib.DeviceItems(wl.items, dev)
+    searcher = _lib.DeviceSearcher(dev)
+    Q, k, L, d_h = len(wl.users), PARAMS["k"], g.n_layers, model.d_h
+    users_d = torch.from_numpy(wl.users).to(f"cuda:{dev}")
+    out_ids = torch.empty((Q, k), dtype=torch.int64, device=f"cuda:{dev}")
+    out_sc = torch.empty((Q, k), dtype=torch.float64, device=f"cuda:{dev}")
+    out_cnt = torch.empty(Q, dtype=torch.int32, device=f"cuda:{dev}")
+    out_st = torch.empty((Q, 5 + L), dtype=torch.int64, device=f"cuda:{dev}")
+    pc = SearchParams(**PARAMS)._c()
+    stream = torch.cuda.current_stream(dev)
+    sp = ctypes.c_void_p(stream.cuda_stream)
+    lib = _lib.lib()
+
+    def step():
+        _lib.check(lib.gr_search_async(searcher.h, g.h, dm.h, it.h, users_d.data_ptr(), Q,
+                                       ctypes.byref(pc), out_ids.data_ptr(), out_sc.data_ptr(),
+                                       out_cnt.data_ptr(), out_st.data_ptr(), sp))
+
+    for _ in range(args.warmup):
+        step()
+    _lib.check(lib.gr_searcher_status(searcher.h, sp))
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize(dev)
+    launches0 = searcher.launches
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    step_ms = []
+    with ClockSampler(dev) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            e_a, e_b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e_a.record(stream)
+            step()
+            e_b.record(stream)
+            step_ms.append((e_a, e_b))
+        ev1.record(stream)
+        torch.cuda.synchronize(dev)
+    _lib.check(lib.gr_searcher_status(searcher.h, sp))
+    launches = searcher.launches - launches0
+    elapsed = ev0.elapsed_time(ev1) / 1000.0
+    per_launch = float(np.mean([a.elapsed_time(b) for a, b in step_ms])) / 1000.0
+    if dist:
+        t = torch.tensor([elapsed], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed = float(t.item())
+    total_q = Q * args.steps * world
+    value = total_q / elapsed
+
+    # ---- per-query work counters of the last step -> algorithmic bytes/flops per launch
+    st = out_st.cpu().numpy()
+    evals, rows, nbrs = st[:, 0], st[:, 3], st[:, 4]
+    bytes_launch = algorithmic_bytes(evals, rows, nbrs, d_h, k)
+    flops_launch = float(evals.sum()) * flops_per_eval(model)
+    pk = peaks()
+    achieved_gbs = bytes_launch / per_launch / 1e9
+    sm_mhz = pk.get("sm_max_mhz", 1965.0)
+    fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # separate fmul/fadd issue, TFLOP/s
+    prof = {}
+    try:
+        prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_search_kernel.json")))
+    except Exception:
+        pass
+    traffic = prof.get("dram_bytes_per_query")
+    roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm_gbs"],
+                "unit": "GB/s", "frac": achieved_gbs / pk["hbm_gbs"],
+                "traffic": None if traffic is None else traffic * Q,
+                "algorithmic_bytes_per_launch": bytes_launch,
+                "peak_source": "MEASURED_PEAKS.json" if "_fallback" not in pk else "fallback",
+                "kernel": "hipanns_search_kernel",
+                "fp32_issue": {"achieved_tflops": flops_launch / per_launch / 1e12,
+                               "peak_tflops": fp32_peak,
+                               "frac": flops_launch / per_launch / 1e12 / fp32_peak,
+                               "note": "exact-fp32 scoring = separately rounded FMUL+FADD "
+                                       "(numpy einsum order), bound by CUDA-core issue"}}
+
+    # ---- e2e through the public API with host buffers (H2D users, D2H results)
+    pin_users = torch.from_numpy(wl.users).pin_memory()
+    h_ids = torch.empty((Q, k), dtype=torch.int64).pin_memory()
+    h_sc = torch.empty((Q, k), dtype=torch.float64).pin_memory()
+    h_cnt = torch.empty(Q, dtype=torch.int32).pin_memory()
+    h_st = torch.empty((Q, 5 + L), dtype=torch.int64).pin_memory()
+
+    def e2e_step():
+        _lib.check(lib.gr_search(searcher.h, g.h, dm.h, it.h, pin_users.data_ptr(), Q,
+                                 ctypes.byref(pc), h_ids.data_ptr(), h_sc.data_ptr(),
+                                 h_cnt.data_ptr(), h_st.data_ptr(), 0, sp))
+
+    e2e_step()
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_step()
+    e2e_t = time.perf_counter() - t0
+    if dist:
+        t = torch.tensor([e2e_t], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_t = float(t.item())
+    h2d = Q * d_h * 4
+    d2h = Q * k * 16 + Q * 4 + Q * (5 + L) * 8
+
+    # ---- recall@100 vs exact brute force (GPU, all items) on a query subset
+    nrec = min(Q, args.recall_queries)
+    gt_ids, _ = brute_force_batch(metric, wl.users[:nrec], wl.items, 100, device=dev)
+    got = h_ids[:nrec].numpy()
+    recall = float(np.mean([len(set(got[q]) & set(gt_ids[q])) / 100.0 for q in range(nrec)]))
+
+    line = {
+        "metric": "queries/sec at recall@100", "value": value, "unit": "queries/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1000 * elapsed / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": config_of(args, wl),
+        "recall_at_100": recall, "recall_queries": nrec,
+        "mean_evals_per_query": float(evals.mean()),
+        "roofline": roofline,
+        "e2e": {"value": total_q / e2e_t, "unit": "queries/s", "h2d_bytes_per_step": h2d,
+                "d2h_bytes_per_step": d2h},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+    }
+    if want_cpu and rank == 0:
+        r, n, t, threads = cpu_baseline(wl, target_s=args.cpu_s)
+        same = np.mean([np.array_equal(r["ids"][q], h_ids[q].numpy()) for q in range(n)])
+        line["cpu_baseline"] = {"value": n / t, "unit": "queries/s", "cores": threads,
+                                "kind": "port",
+                                "sample": f"first {n} queries of the batch, oracle/c (C "
+                                          f"restatement of nann.c_hipanns + einsum-order "
+                                          f"relevance), {threads} threads, {t:.1f}s"}
+        line["ids_identical_to_cpu_reference"] = float(same)
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="gmpgr", choices=["gmpgr", "reference"])
+    ap.add_argument("--config", default="cfg3", choices=["cfg1", "cfg2", "cfg3", "small"])
+    ap.add_argument("--recall-queries", type=int, default=256)
+    ap.add_argument("--cpu-s", type=float, default=15.0)
+    ap.add_argument("--ref-step-s", type=float, default=8.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_gmpgr(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

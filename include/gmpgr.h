@@ -1,0 +1,141 @@
+/*
+ * gmpgr.h — C ABI of the B200-native GMP-GR HiPANNS retrieval hot path.
+ *
+ * libgmpgr.so (paper_2502_11490_b200/csrc, built for sm_100a) exports exactly the
+ * functions below.  Plain pointers and sizes only; no torch types.  Every entry
+ * point returns GR_OK (0) or an error code; gr_last_error() gives the message
+ * (thread-local).  The Python package maps codes to the reference's exception
+ * classes (errors.py:8-59): GR_EINVAL -> InvalidArgumentError,
+ * GR_ENUMERIC -> NumericError, GR_ECUDA/GR_ENOMEM -> RuntimeError/MemoryError.
+ *
+ * Reference interfaces each entry point replaces (file:line under
+ * /root/reference/pkg/src/nann/):
+ *   gr_model_create   <- MetricModel / RelevanceModel weights (metric.py:74-99, 192-226),
+ *                        NANN-MODEL payload order (metric.py:310-399)
+ *   gr_graph_create   <- GraphIndex.graph_view() (index.py:384-391), NANN-IDX (index.py:397-508)
+ *   gr_items_create   <- model_scorer's item_embeddings (search.py:84-90)
+ *   gr_score_pairs    <- ScoreFn (search.py:27) / RelevanceModel.score (metric.py:222-226) /
+ *                        BatchEngine.evaluate (batching.py:67-109) / relevance_batch (metric.py:150-154)
+ *   gr_search         <- c_hipanns(index, model_scorer(model, h_u, emb), SearchParams)
+ *                        (search.py:194-286, 30-70), batched over Q user embeddings
+ *   gr_brute_force    <- brute_force(model_scorer(...), ids, k) (search.py:93-108)
+ *   gr_merge_topk     <- CandidatePool(k).push(...) over several result lists (pool.py:11-55)
+ *
+ * Pointer arguments documented "host-or-device" follow the `on_device` flag of
+ * the call: 0 = host memory (the library copies in/out on `stream` and
+ * synchronises), 1 = device memory on the handle's device (asynchronous on
+ * `stream` except where a status must be read back; see each call).
+ */
+#ifndef GMPGR_H
+#define GMPGR_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum {
+    GR_OK = 0,
+    GR_EINVAL = 1,   /* bad argument / contract violation */
+    GR_ENUMERIC = 2, /* non-finite metric output (metric.py:134-135) */
+    GR_ECUDA = 3,    /* CUDA runtime failure */
+    GR_ENOMEM = 4    /* device allocation failure */
+};
+
+#define GR_ABI_VERSION 1
+
+typedef struct gr_model gr_model;
+typedef struct gr_graph gr_graph;
+typedef struct gr_items gr_items;
+typedef struct gr_searcher gr_searcher;
+
+/* Search knobs = SearchParams (search.py:30-49); ef is frontier_width (ef or 2k). */
+typedef struct {
+    int32_t k;
+    int32_t k_parallel;
+    int32_t hops;
+    int32_t ef;
+} gr_search_params;
+
+const char *gr_last_error(void);
+int gr_abi_version(void);
+/* number of CUDA devices visible (0 without a GPU; never fails) */
+int gr_device_count(void);
+
+/* Metric MLP.  n_mlp layers; dims[0] = 2*d_h (pair width), dims[m+1] = output width of
+ * layer m, dims[n_mlp] = z_dim.  W[m]: host fp32 row-major [dims[m+1], dims[m]] (the
+ * reference's (d_out, d_in) layout); b[m]: [dims[m+1]]; attention: [z_dim]; relu: 1 for
+ * "relu" (ReLU between layers, never after the last), 0 for "identity".  fp16 models are
+ * passed widened to fp32 (exact). */
+int gr_model_create(int device, int n_mlp, const int32_t *dims, const float *const *W,
+                    const float *const *b, const float *attention, int relu, gr_model **out);
+int gr_model_destroy(gr_model *m);
+
+/* Layered graph over n slots.  For layer l < n_layers: nbrs[l] host int32 rows of
+ * row_stride[l] entries (the first cnts[l][s] of row s are neighbour SLOTS; the reference's
+ * fixed-width _nbrs[l] arrays, index.py:78-79); levels host int32 [n] (node level, index.py:77);
+ * entry_slot (index.py:68); ids host int64 [n] (item id per slot: output ids and the
+ * (score desc, id asc) tie-break); rows host int32 [n] or NULL: embedding row per slot
+ * (NULL -> rows = ids, the model_scorer convention search.py:88). */
+int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *nbrs,
+                    const int64_t *row_stride, const int32_t *const *cnts, const int32_t *levels,
+                    int32_t entry_slot, const int64_t *ids, const int32_t *rows, gr_graph **out);
+int gr_graph_destroy(gr_graph *g);
+
+/* Item embeddings fp32 [n, d] row-major (host or device pointer per emb_on_device). */
+int gr_items_create(int device, const float *emb, int64_t n, int32_t d, int emb_on_device,
+                    gr_items **out);
+int gr_items_destroy(gr_items *it);
+
+/* Relevance of n (user, item) pairs (relevance_batch bit-exact).  users fp32 [n_users, d_h];
+ * user_index int32 [n] (NULL -> every pair uses users[0], the model_scorer broadcast);
+ * item_ids int64 [n] (rows of the items handle); out fp64 [n].  host-or-device pointers.
+ * Synchronous; returns GR_ENUMERIC if any final-layer output is non-finite. */
+int gr_score_pairs(const gr_model *m, const gr_items *it, const float *users, int64_t n_users,
+                   const int32_t *user_index, const int64_t *item_ids, int64_t n,
+                   double *out_scores, int on_device, void *stream);
+
+/* Scratch owner for gr_search (visited tags, frontiers, pools).  One per stream. */
+int gr_searcher_create(int device, gr_searcher **out);
+int gr_searcher_destroy(gr_searcher *s);
+
+/* Batched C-HiPANNS, deterministic lock-step semantics, exact fp32 scoring.
+ * users fp32 [Q, d_h].  Outputs: ids int64 [Q, k] (-1 padded), scores fp64 [Q, k],
+ * count int32 [Q], stats int64 [Q, 5 + n_layers] = (metric_evaluations, nodes_visited,
+ * hops_to_best or -1, adjacency rows expanded, neighbour ids read, per-layer evaluations
+ * base layer first).  host-or-device pointers.
+ * Synchronous (reads back the numeric flag); GR_ENUMERIC on a non-finite metric output. */
+int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_items *it,
+              const float *users, int64_t Q, const gr_search_params *p, int64_t *out_ids,
+              double *out_scores, int32_t *out_count, int64_t *out_stats, int on_device,
+              void *stream);
+
+/* Same as gr_search but asynchronous on `stream` with device pointers only; the numeric
+ * flag is accumulated in the searcher and returned by gr_searcher_status. */
+int gr_search_async(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_items *it,
+                    const float *users, int64_t Q, const gr_search_params *p, int64_t *out_ids,
+                    double *out_scores, int32_t *out_count, int64_t *out_stats, void *stream);
+/* Synchronise `stream`, return GR_ENUMERIC if any async search saw a non-finite output
+ * since the last call (and clear the flag), else GR_OK. */
+int gr_searcher_status(gr_searcher *s, void *stream);
+/* kernel launches issued by this searcher so far (evidence counter for bench.py) */
+int64_t gr_searcher_launches(const gr_searcher *s);
+
+/* Exact top-k over ALL items of the handle for Q users (ground truth, search.py:93-108):
+ * ids int64 [Q, k] (= item rows), scores fp64 [Q, k].  host-or-device pointers. */
+int gr_brute_force(const gr_model *m, const gr_items *it, const float *users, int64_t Q,
+                   int32_t k, int64_t *out_ids, double *out_scores, int on_device, void *stream);
+
+/* Merge R per-shard top-k lists per query into one top-k by (score desc, id asc)
+ * (CandidatePool.push of every entry, pool.py:30-55).  in_ids/in_scores [R, Q, k_in]
+ * (-1 ids are empty slots), out [Q, k].  Device pointers, asynchronous. */
+int gr_merge_topk(int device, const int64_t *in_ids, const double *in_scores, int32_t R,
+                  int64_t Q, int32_t k_in, int32_t k, int64_t *out_ids, double *out_scores,
+                  int32_t *out_count, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GMPGR_H */

@@ -194,6 +194,7 @@ static void search1(const ograph *g, const omodel *m, const float *items, int d,
     w->epoch++;
     w->n_scored = 0;
     int64_t evals = 0, per_layer[OMAX_LAYERS] = {0};
+    int64_t rows = 0, nbr_ids = 0; /* _neighbors_of calls / ids returned (search.py:135-137) */
     int kp = P->kp, ef = P->ef;
 
 #define SCORE_SLOT(s, hop)                                                                   \
@@ -210,6 +211,8 @@ static void search1(const ograph *g, const omodel *m, const float *items, int d,
         w->claimed[s0] = w->epoch;
         SCORE_SLOT(s0, 0);
         const int32_t *row = g->nbrs[top] + (size_t)s0 * g->stride[top];
+        rows += 1;
+        nbr_ids += g->cnts[top][s0];
         for (int j = 0; j < g->cnts[top][s0]; ++j) {
             int32_t v = row[j];
             if (w->claimed[v] == w->epoch) continue;
@@ -239,6 +242,8 @@ static void search1(const ograph *g, const omodel *m, const float *items, int d,
                 for (int f = 0; f < w->fcount[i]; ++f) {
                     int32_t s = w->frontier[w->foff[i] + f];
                     const int32_t *row = nb + (size_t)s * st;
+                    rows += 1;
+                    nbr_ids += ct[s];
                     for (int j = 0; j < ct[s]; ++j) {
                         int32_t v = row[j];
                         if (w->claimed[v] == w->epoch || w->seen[v] == w->hstamp) continue;
@@ -276,14 +281,17 @@ static void search1(const ograph *g, const omodel *m, const float *items, int d,
     stats[0] = evals;
     stats[1] = evals;
     stats[2] = nr ? seeds[0].hop : -1;
-    for (int l = 0; l < g->n_layers; ++l) stats[3 + l] = per_layer[l];
+    stats[3] = rows;
+    stats[4] = nbr_ids;
+    for (int l = 0; l < g->n_layers; ++l) stats[5 + l] = per_layer[l];
 #undef SCORE_SLOT
 }
 
 /*
  * Batched search, one query per OpenMP task.  Output layout:
  *   out_ids[Q, k] int64, out_scores[Q, k] f64, out_n[Q],
- *   stats[Q, 3 + n_layers] = evals, nodes_visited, hops_to_best, per-layer evals.
+ *   stats[Q, 5 + n_layers] = evals, nodes_visited, hops_to_best, rows expanded,
+ *   neighbour ids read, per-layer evals.
  * Returns 0, or 2 if any final-layer metric output was non-finite.
  */
 int oracle_search(int n_layers, int64_t n, const int32_t *const *nbrs, const int64_t *stride,
@@ -309,7 +317,7 @@ int oracle_search(int n_layers, int64_t n, const int32_t *const *nbrs, const int
     if (cap_fresh > n) cap_fresh = n;
     cap_fresh += 64;
     int bad = 0;
-    int nst = 3 + n_layers;
+    int nst = 5 + n_layers;
 #pragma omp parallel num_threads(nthreads > 0 ? nthreads : 1) reduction(| : bad)
     {
         owork w;

@@ -88,7 +88,7 @@ def search(layers, entry_slot, ids, model_layers, attention, relu, items, users,
     out_ids = np.full((Q, k), -1, dtype=np.int64)
     out_scores = np.full((Q, k), np.nan)
     out_n = np.zeros(Q, dtype=np.int32)
-    stats = np.zeros((Q, 3 + L), dtype=np.int64)
+    stats = np.zeros((Q, 5 + L), dtype=np.int64)
     rc = lib().oracle_search(
         C.c_int(L), C.c_int64(len(ids)), _ptr_array(nbrs), _ptr(stride), _ptr_array(cnts),
         C.c_int32(int(entry_slot)), _ptr(ids), _ptr(rank),
@@ -100,4 +100,5 @@ def search(layers, entry_slot, ids, model_layers, attention, relu, items, users,
     if rc == 1:
         raise ValueError("oracle_search: bad arguments")
     return dict(ids=out_ids, scores=out_scores, n=out_n, evals=stats[:, 0], visited=stats[:, 1],
-                best_hop=stats[:, 2], per_layer=stats[:, 3:], finite=rc == 0)
+                best_hop=stats[:, 2], rows=stats[:, 3], nbr_ids=stats[:, 4],
+                per_layer=stats[:, 5:], finite=rc == 0)

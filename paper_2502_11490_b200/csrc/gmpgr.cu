@@ -1,0 +1,859 @@
+// libgmpgr.so — C ABI (include/gmpgr.h) over the sm_100a HiPANNS kernels.
+//
+// Host side: handle construction (processing-order weight packing, compact
+// device graph layout, padded item rows), scratch management and launches.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <numeric>
+#include <string>
+#include <vector>
+
+#include "../../include/gmpgr.h"
+#include "aux_kernels.cuh"
+#include "common.cuh"
+#include "search_kernel.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string &msg) {
+    g_err = msg;
+    return code;
+}
+
+#define GR_CUDA(call)                                                                       \
+    do {                                                                                    \
+        cudaError_t e_ = (call);                                                            \
+        if (e_ != cudaSuccess) {                                                            \
+            return fail(e_ == cudaErrorMemoryAllocation ? GR_ENOMEM : GR_ECUDA,             \
+                        std::string(#call) + ": " + cudaGetErrorString(e_));                \
+        }                                                                                   \
+    } while (0)
+
+int round4(int x) { return (x + 3) & ~3; }
+int odd(int x) { return x | 1; }
+int pow2ceil(int x) {
+    int p = 32;
+    while (p < x) p <<= 1;
+    return p;
+}
+
+template <class T>
+int dmalloc(T **p, size_t count) {
+    if (count == 0) count = 1;
+    cudaError_t e = cudaMalloc(reinterpret_cast<void **>(p), count * sizeof(T));
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(GR_ENOMEM, std::string("cudaMalloc ") + std::to_string(count * sizeof(T)) +
+                                   " bytes: " + cudaGetErrorString(e));
+    }
+    return GR_OK;
+}
+
+struct DevBuf {
+    void *p = nullptr;
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+    }
+};
+
+int num_sms(int device) {
+    int n = 0;
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device);
+    return n > 0 ? n : 1;
+}
+
+} // namespace
+
+// ------------------------------------------------------------------ handles
+struct gr_model {
+    int device;
+    DevModel dm;
+    void *dbuf;
+    std::vector<int> dims;
+};
+
+struct gr_graph {
+    int device;
+    DevGraph dg;
+    std::vector<void *> bufs;
+    int max_deg;
+};
+
+struct gr_items {
+    int device;
+    DevItems di;
+    void *dbuf;
+};
+
+struct gr_searcher {
+    int device;
+    int64_t slots = 0, n = 0, capF = 0, capS = 0, capP = 0;
+    uint64_t *tags = nullptr;
+    uint32_t *epochs = nullptr;
+    int32_t *f_slot = nullptr, *f_srch = nullptr, *surv_v = nullptr, *surv_i = nullptr,
+            *fr_v = nullptr, *fr_i = nullptr, *seg_v = nullptr, *pool_slot = nullptr;
+    uint64_t *fr_key = nullptr, *seg_key = nullptr, *pool_key = nullptr;
+    int *flags = nullptr; // [0] queue, [1] nonfinite, [2] bad index
+    int64_t launches = 0;
+    // staging for host-pointer calls
+    DevBuf st_users, st_ids, st_scores, st_count, st_stats;
+    size_t st_users_n = 0, st_out_n = 0, st_stats_n = 0;
+    void free_scratch() {
+        void *ps[] = {tags, epochs, f_slot, f_srch, surv_v, surv_i, fr_v, fr_i, seg_v, pool_slot,
+                      fr_key, seg_key, pool_key};
+        for (void *p : ps)
+            if (p) cudaFree(p);
+        tags = nullptr; epochs = nullptr; f_slot = f_srch = surv_v = surv_i = fr_v = fr_i = seg_v =
+            pool_slot = nullptr;
+        fr_key = seg_key = pool_key = nullptr;
+        slots = n = capF = capS = capP = 0;
+    }
+};
+
+extern "C" {
+
+const char *gr_last_error(void) { return g_err.c_str(); }
+int gr_abi_version(void) { return GR_ABI_VERSION; }
+int gr_device_count(void) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess) {
+        cudaGetLastError();
+        return 0;
+    }
+    return n;
+}
+
+// ------------------------------------------------------------------ model
+int gr_model_create(int device, int n_mlp, const int32_t *dims, const float *const *W,
+                    const float *const *b, const float *attention, int relu, gr_model **out) {
+    if (!out || !dims || !W || !b || !attention) return fail(GR_EINVAL, "null argument");
+    if (n_mlp < 1 || n_mlp > GR_MAX_MLP) return fail(GR_EINVAL, "n_mlp out of range [1, 6]");
+    if (dims[0] < 2 || dims[0] % 2) return fail(GR_EINVAL, "dims[0] must be 2*d_h");
+    for (int m = 0; m <= n_mlp; ++m)
+        if (dims[m] < 1 || dims[m] > 2048) return fail(GR_EINVAL, "layer width out of range");
+    GR_CUDA(cudaSetDevice(device));
+    // processing-order packing (common.cuh)
+    std::vector<float> host;
+    std::vector<size_t> offW(n_mlp), offb(n_mlp);
+    for (int m = 0; m < n_mlp; ++m) {
+        const int K = dims[m], O = dims[m + 1], nch = n_chunks(K);
+        offW[m] = host.size();
+        host.resize(host.size() + (size_t)nch * O * 4, 0.f);
+        float *dst = host.data() + offW[m];
+        for (int j = 0; j < nch; ++j) {
+            const int c = chunk_perm(j, K);
+            for (int o = 0; o < O; ++o)
+                for (int u = 0; u < 4; ++u) {
+                    const int kk = 4 * c + u;
+                    dst[((size_t)j * O + o) * 4 + u] = kk < K ? W[m][(size_t)o * K + kk] : 0.f;
+                }
+        }
+        offb[m] = host.size();
+        host.resize(host.size() + round4(O), 0.f);
+        std::memcpy(host.data() + offb[m], b[m], sizeof(float) * O);
+    }
+    const int Z = dims[n_mlp], nchA = n_chunks(Z);
+    const size_t offA = host.size();
+    host.resize(host.size() + (size_t)nchA * 4, 0.f);
+    for (int j = 0; j < nchA; ++j) {
+        const int c = chunk_perm(j, Z);
+        for (int u = 0; u < 4; ++u) {
+            const int kk = 4 * c + u;
+            host[offA + (size_t)j * 4 + u] = kk < Z ? attention[kk] : 0.f;
+        }
+    }
+    gr_model *M = new gr_model();
+    M->device = device;
+    M->dims.assign(dims, dims + n_mlp + 1);
+    float *d = nullptr;
+    int rc = dmalloc(&d, host.size());
+    if (rc) { delete M; return rc; }
+    cudaError_t e = cudaMemcpy(d, host.data(), host.size() * sizeof(float), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(d); delete M; return fail(GR_ECUDA, cudaGetErrorString(e)); }
+    M->dbuf = d;
+    DevModel &dm = M->dm;
+    std::memset(&dm, 0, sizeof(dm));
+    dm.n_mlp = n_mlp;
+    dm.relu = relu ? 1 : 0;
+    dm.d_h = dims[0] / 2;
+    dm.Z = Z;
+    for (int m = 0; m <= n_mlp; ++m) { dm.dims[m] = dims[m]; dm.nch[m] = n_chunks(dims[m]); }
+    for (int m = 0; m < n_mlp; ++m) {
+        dm.W[m] = reinterpret_cast<const float4 *>(d + offW[m]);
+        dm.b[m] = d + offb[m];
+    }
+    dm.A = reinterpret_cast<const float4 *>(d + offA);
+    dm.pre_ch = 4 * (dm.d_h / 16);
+    *out = M;
+    return GR_OK;
+}
+
+int gr_model_destroy(gr_model *m) {
+    if (!m) return GR_OK;
+    cudaSetDevice(m->device);
+    cudaFree(m->dbuf);
+    delete m;
+    return GR_OK;
+}
+
+// ------------------------------------------------------------------ graph
+int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *nbrs,
+                    const int64_t *row_stride, const int32_t *const *cnts, const int32_t *levels,
+                    int32_t entry_slot, const int64_t *ids, const int32_t *rows, gr_graph **out) {
+    if (!out || !nbrs || !row_stride || !cnts || !ids) return fail(GR_EINVAL, "null argument");
+    if (n < 1) return fail(GR_EINVAL, "index is empty");
+    if (n > 0x7ffffff0LL) return fail(GR_EINVAL, "more than 2^31 slots");
+    if (n_layers < 1 || n_layers > GR_MAX_LAYERS) return fail(GR_EINVAL, "n_layers out of range [1, 8]");
+    if (entry_slot < 0 || entry_slot >= n) return fail(GR_EINVAL, "entry_slot out of range");
+    GR_CUDA(cudaSetDevice(device));
+    gr_graph *G = new gr_graph();
+    G->device = device;
+    DevGraph &dg = G->dg;
+    std::memset(&dg, 0, sizeof(dg));
+    dg.n_layers = n_layers;
+    dg.n = n;
+    dg.entry = entry_slot;
+    G->max_deg = 0;
+    auto cleanup = [&](int rc) {
+        for (void *p : G->bufs) cudaFree(p);
+        delete G;
+        return rc;
+    };
+    // upper-layer membership: level >= 1 (index.py:77, nesting); fall back to "has edges"
+    std::vector<int32_t> up_row(n, -1);
+    int64_t n_up = 0;
+    if (n_layers > 1) {
+        for (int64_t s = 0; s < n; ++s) {
+            bool member = levels ? levels[s] >= 1 : false;
+            if (!levels)
+                for (int l = 1; l < n_layers; ++l) member |= cnts[l][s] > 0;
+            if (member) up_row[s] = (int32_t)n_up++;
+        }
+    }
+    for (int l = 0; l < n_layers; ++l) {
+        const int64_t stride = row_stride[l];
+        if (stride < 0 || stride > 4096) return cleanup(fail(GR_EINVAL, "row stride out of range"));
+        const int deg = (int)std::max<int64_t>(stride, 1);
+        const int ld = round4(deg);
+        const int64_t nrows = l == 0 ? n : std::max<int64_t>(n_up, 1);
+        std::vector<int32_t> h((size_t)nrows * ld, -1);
+        for (int64_t s = 0; s < n; ++s) {
+            const int32_t c = cnts[l][s];
+            if (c == 0) continue;
+            if (c < 0 || c > stride)
+                return cleanup(fail(GR_EINVAL, "layer " + std::to_string(l) + " slot " +
+                                                   std::to_string(s) + ": bad neighbour count"));
+            int64_t r = l == 0 ? s : up_row[s];
+            if (r < 0) continue; // not a member of this layer: never expanded
+            const int32_t *src = nbrs[l] + s * stride;
+            for (int j = 0; j < c; ++j) {
+                if (src[j] < 0 || src[j] >= n)
+                    return cleanup(fail(GR_EINVAL, "neighbour slot out of range"));
+                h[(size_t)r * ld + j] = src[j];
+            }
+        }
+        int32_t *d = nullptr;
+        if (int rc = dmalloc(&d, h.size())) return cleanup(rc);
+        G->bufs.push_back(d);
+        if (cudaMemcpy(d, h.data(), h.size() * 4, cudaMemcpyHostToDevice) != cudaSuccess)
+            return cleanup(fail(GR_ECUDA, "graph upload failed"));
+        dg.adj[l] = d;
+        dg.ld[l] = ld;
+        dg.deg[l] = deg;
+        G->max_deg = std::max(G->max_deg, deg);
+    }
+    {
+        int32_t *d = nullptr;
+        if (int rc = dmalloc(&d, n)) return cleanup(rc);
+        G->bufs.push_back(d);
+        cudaMemcpy(d, up_row.data(), n * 4, cudaMemcpyHostToDevice);
+        dg.up_row = d;
+    }
+    {
+        int64_t *d = nullptr;
+        if (int rc = dmalloc(&d, n)) return cleanup(rc);
+        G->bufs.push_back(d);
+        cudaMemcpy(d, ids, n * 8, cudaMemcpyHostToDevice);
+        dg.ids = d;
+    }
+    // embedding rows: explicit, else ids (model_scorer convention); identity -> nullptr
+    {
+        std::vector<int32_t> r(n);
+        bool ident = true;
+        for (int64_t s = 0; s < n; ++s) {
+            const int64_t v = rows ? (int64_t)rows[s] : ids[s];
+            if (v < 0 || v > 0x7fffffffLL)
+                return cleanup(fail(GR_EINVAL, "item ids must be row indexes >= 0 (search.py:84-90)"));
+            r[s] = (int32_t)v;
+            ident &= (v == s);
+        }
+        if (!ident) {
+            int32_t *d = nullptr;
+            if (int rc = dmalloc(&d, n)) return cleanup(rc);
+            G->bufs.push_back(d);
+            cudaMemcpy(d, r.data(), n * 4, cudaMemcpyHostToDevice);
+            dg.rows = d;
+        }
+    }
+    // tie-break rank: slot when ids ascend, else rank of id
+    {
+        bool mono = true;
+        for (int64_t s = 1; s < n && mono; ++s) mono = ids[s] > ids[s - 1];
+        if (!mono) {
+            std::vector<int64_t> order(n);
+            std::iota(order.begin(), order.end(), 0);
+            std::stable_sort(order.begin(), order.end(),
+                             [&](int64_t a, int64_t b) { return ids[a] < ids[b]; });
+            std::vector<uint32_t> rank(n);
+            for (int64_t i = 0; i < n; ++i) rank[order[i]] = (uint32_t)i;
+            uint32_t *d = nullptr;
+            if (int rc = dmalloc(&d, n)) return cleanup(rc);
+            G->bufs.push_back(d);
+            cudaMemcpy(d, rank.data(), n * 4, cudaMemcpyHostToDevice);
+            dg.rank = d;
+        }
+    }
+    GR_CUDA(cudaDeviceSynchronize());
+    *out = G;
+    return GR_OK;
+}
+
+int gr_graph_destroy(gr_graph *g) {
+    if (!g) return GR_OK;
+    cudaSetDevice(g->device);
+    for (void *p : g->bufs) cudaFree(p);
+    delete g;
+    return GR_OK;
+}
+
+// ------------------------------------------------------------------ items
+int gr_items_create(int device, const float *emb, int64_t n, int32_t d, int emb_on_device,
+                    gr_items **out) {
+    if (!out || !emb) return fail(GR_EINVAL, "null argument");
+    if (n < 1 || d < 1) return fail(GR_EINVAL, "empty item embeddings");
+    GR_CUDA(cudaSetDevice(device));
+    const int ld = round4(d);
+    float *p = nullptr;
+    if (int rc = dmalloc(&p, (size_t)n * ld)) return rc;
+    if (ld != d) cudaMemset(p, 0, (size_t)n * ld * 4);
+    cudaError_t e = cudaMemcpy2D(p, (size_t)ld * 4, emb, (size_t)d * 4, (size_t)d * 4, n,
+                                 emb_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(p); return fail(GR_ECUDA, cudaGetErrorString(e)); }
+    gr_items *I = new gr_items();
+    I->device = device;
+    I->di.emb = p;
+    I->di.n = n;
+    I->di.d = d;
+    I->di.ld = ld;
+    I->dbuf = p;
+    *out = I;
+    return GR_OK;
+}
+
+int gr_items_destroy(gr_items *it) {
+    if (!it) return GR_OK;
+    cudaSetDevice(it->device);
+    cudaFree(it->dbuf);
+    delete it;
+    return GR_OK;
+}
+
+} // extern "C"
+
+// ------------------------------------------------------------------ layouts
+namespace {
+
+struct SmemPlan {
+    int bytes = 0;
+    int alloc(int nbytes) {
+        int off = bytes;
+        bytes += (nbytes + 15) & ~15;
+        return off;
+    }
+};
+
+// weights for layers >= 1 + biases + attention (shared by all kernels)
+void plan_weights(const DevModel &M, SmemPlan &P, int *off_w, int *off_b, int *off_A) {
+    for (int m = 0; m < M.n_mlp; ++m) {
+        off_w[m] = m >= 1 ? P.alloc(M.nch[m] * M.dims[m + 1] * 16) : 0;
+        off_b[m] = P.alloc(round4(M.dims[m + 1]) * 4);
+    }
+    *off_A = P.alloc(M.nch[M.n_mlp] * 16);
+}
+
+int hidden_ld(const DevModel &M) {
+    int mx = 1;
+    for (int m = 1; m <= M.n_mlp; ++m) mx = std::max(mx, M.nch[m]);
+    return odd(mx);
+}
+
+int plan_search(const DevModel &M, int k, int kp, SearchArgs &a) {
+    SmemPlan P;
+    const int x0_nch = M.nch[0] - M.pre_ch;
+    a.off_w0 = P.alloc(x0_nch * M.dims[1] * 16);
+    plan_weights(M, P, a.off_w, a.off_b, &a.off_A);
+    a.off_acc0 = P.alloc(M.dims[1] * 16);
+    a.ldx0 = odd(x0_nch);
+    a.off_x0 = P.alloc(GR_PT * a.ldx0 * 16);
+    a.ldh = hidden_ld(M);
+    a.off_h0 = P.alloc(GR_PT * a.ldh * 16);
+    a.off_h1 = P.alloc(GR_PT * a.ldh * 16);
+    a.off_score = P.alloc(GR_PT * 4);
+    a.off_hist = P.alloc(GR_NW * 256 * 4);
+    a.sortcap = pow2ceil(std::max(k, kp));
+    a.off_sortk = P.alloc(a.sortcap * 8);
+    a.off_sortv = P.alloc(a.sortcap * 4);
+    a.off_kp = P.alloc(3 * kp * 4);
+    return P.bytes;
+}
+
+int plan_pairs(const DevModel &M, PairArgs &a) {
+    SmemPlan P;
+    for (int m = 0; m < M.n_mlp; ++m) {
+        a.off_w[m] = P.alloc(M.nch[m] * M.dims[m + 1] * 16);
+        a.off_b[m] = P.alloc(round4(M.dims[m + 1]) * 4);
+    }
+    a.off_A = P.alloc(M.nch[M.n_mlp] * 16);
+    a.ldx0 = odd(M.nch[0]);
+    a.off_x0 = P.alloc(GR_PT * a.ldx0 * 16);
+    a.ldh = hidden_ld(M);
+    a.off_h0 = P.alloc(GR_PT * a.ldh * 16);
+    a.off_h1 = P.alloc(GR_PT * a.ldh * 16);
+    a.off_score = P.alloc(GR_PT * 4);
+    return P.bytes;
+}
+
+int plan_brute(const DevModel &M, BruteArgs &a) {
+    SmemPlan P;
+    const int x0_nch = M.nch[0] - M.pre_ch;
+    a.off_w0 = P.alloc(x0_nch * M.dims[1] * 16);
+    plan_weights(M, P, a.off_w, a.off_b, &a.off_A);
+    a.off_acc0 = P.alloc(M.dims[1] * 16);
+    a.ldx0 = odd(x0_nch);
+    a.off_x0 = P.alloc(GR_PT * a.ldx0 * 16);
+    a.ldh = hidden_ld(M);
+    a.off_h0 = P.alloc(GR_PT * a.ldh * 16);
+    a.off_h1 = P.alloc(GR_PT * a.ldh * 16);
+    a.off_score = P.alloc(GR_PT * 4);
+    a.off_hist = P.alloc(256 * 4);
+    return P.bytes;
+}
+
+const int kMaxSmem = 227 * 1024;
+
+template <class K>
+int set_smem(K kernel, int bytes) {
+    if (bytes > kMaxSmem) return fail(GR_EINVAL, "model too large for shared memory");
+    GR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    return GR_OK;
+}
+
+// staging helper for host-pointer calls
+template <class T>
+int stage(DevBuf &buf, size_t &cap, size_t count) {
+    if (count <= cap && buf.p) return GR_OK;
+    buf.release();
+    T *p = nullptr;
+    if (int rc = dmalloc(&p, count)) return rc;
+    buf.p = p;
+    cap = count;
+    return GR_OK;
+}
+
+int ensure_search_scratch(gr_searcher *S, const gr_graph *G, int64_t slots, int64_t capF,
+                          int64_t capS, int64_t capP) {
+    const int64_t n = G->dg.n;
+    if (S->slots >= slots && S->n == n && S->capF >= capF && S->capS >= capS && S->capP >= capP)
+        return GR_OK;
+    slots = std::max(slots, S->slots);
+    capF = std::max(capF, S->capF);
+    capS = std::max(capS, S->capS);
+    capP = std::max(capP, S->capP);
+    S->free_scratch();
+    int rc = GR_OK;
+    if ((rc = dmalloc(&S->tags, (size_t)slots * n))) return rc;
+    if ((rc = dmalloc(&S->epochs, (size_t)slots))) return rc;
+    if ((rc = dmalloc(&S->f_slot, (size_t)slots * 2 * capF))) return rc;
+    if ((rc = dmalloc(&S->f_srch, (size_t)slots * 2 * capF))) return rc;
+    if ((rc = dmalloc(&S->surv_v, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->surv_i, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->fr_v, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->fr_i, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->fr_key, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->seg_v, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->seg_key, (size_t)slots * capS))) return rc;
+    if ((rc = dmalloc(&S->pool_key, (size_t)slots * 2 * capP))) return rc;
+    if ((rc = dmalloc(&S->pool_slot, (size_t)slots * 2 * capP))) return rc;
+    GR_CUDA(cudaMemset(S->tags, 0, (size_t)slots * n * 8));
+    GR_CUDA(cudaMemset(S->epochs, 0, (size_t)slots * 4));
+    S->slots = slots;
+    S->n = n;
+    S->capF = capF;
+    S->capS = capS;
+    S->capP = capP;
+    return GR_OK;
+}
+
+int check_params(const gr_search_params *p) {
+    if (!p) return fail(GR_EINVAL, "null params");
+    if (p->k < 1 || p->k_parallel < 1 || p->hops < 1)
+        return fail(GR_EINVAL, "k, k_parallel, and hops must be >= 1");
+    if (p->k_parallel > p->k) return fail(GR_EINVAL, "k_parallel must not exceed k");
+    if (p->ef < 1) return fail(GR_EINVAL, "ef must be >= 1");
+    if (p->k > 8192) return fail(GR_EINVAL, "k > 8192 not supported on the device path");
+    return GR_OK;
+}
+
+int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I,
+                  const float *users, int64_t Q, const gr_search_params *p, int64_t *ids,
+                  double *scores, int32_t *count, int64_t *stats, cudaStream_t stream) {
+    if (M->dm.d_h != I->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
+    SearchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    const int smem = plan_search(M->dm, p->k, p->k_parallel, a);
+    const bool two = smem <= 110 * 1024;
+    if (two) {
+        if (int rc = set_smem(hipanns_search_kernel<2>, smem)) return rc;
+    } else {
+        if (int rc = set_smem(hipanns_search_kernel<1>, smem)) return rc;
+    }
+    int per_sm = 0;
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
+        &per_sm, two ? hipanns_search_kernel<2> : hipanns_search_kernel<1>, GR_NT, smem));
+    if (per_sm < 1) return fail(GR_EINVAL, "search kernel does not fit on an SM");
+    int64_t slots = std::min<int64_t>(Q, (int64_t)per_sm * num_sms(G->device));
+    const int64_t capF = (int64_t)p->k_parallel * p->ef;
+    int64_t capS = std::min<int64_t>(capF * G->max_deg, (int64_t)p->k_parallel * G->dg.n);
+    capS = std::max<int64_t>(capS, G->max_deg + 1) + 64;
+    const int64_t capP = p->k + capS;
+    if (int rc = ensure_search_scratch(S, G, slots, capF, capS, capP)) return rc;
+    a.g = G->dg;
+    a.M = M->dm;
+    a.it = I->di;
+    a.users = users;
+    a.Q = Q;
+    a.k = p->k;
+    a.kp = p->k_parallel;
+    a.hops = p->hops;
+    a.ef = p->ef;
+    a.out_ids = ids;
+    a.out_scores = scores;
+    a.out_count = count;
+    a.out_stats = stats;
+    a.tags = S->tags;
+    a.epochs = S->epochs;
+    a.f_slot = S->f_slot;
+    a.f_srch = S->f_srch;
+    a.surv_v = S->surv_v;
+    a.surv_i = S->surv_i;
+    a.fr_v = S->fr_v;
+    a.fr_i = S->fr_i;
+    a.fr_key = S->fr_key;
+    a.seg_v = S->seg_v;
+    a.seg_key = S->seg_key;
+    a.pool_key = S->pool_key;
+    a.pool_slot = S->pool_slot;
+    a.capF = S->capF;
+    a.capS = S->capS;
+    a.capP = S->capP;
+    a.queue = S->flags;
+    a.nonfinite = S->flags + 1;
+    GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
+    if (two)
+        hipanns_search_kernel<2><<<(int)slots, GR_NT, smem, stream>>>(a);
+    else
+        hipanns_search_kernel<1><<<(int)slots, GR_NT, smem, stream>>>(a);
+    GR_CUDA(cudaGetLastError());
+    S->launches += 1;
+    return GR_OK;
+}
+
+} // namespace
+
+extern "C" {
+
+int gr_searcher_create(int device, gr_searcher **out) {
+    if (!out) return fail(GR_EINVAL, "null argument");
+    GR_CUDA(cudaSetDevice(device));
+    gr_searcher *S = new gr_searcher();
+    S->device = device;
+    if (int rc = dmalloc(&S->flags, 4)) { delete S; return rc; }
+    cudaMemset(S->flags, 0, 16);
+    *out = S;
+    return GR_OK;
+}
+
+int gr_searcher_destroy(gr_searcher *s) {
+    if (!s) return GR_OK;
+    cudaSetDevice(s->device);
+    s->free_scratch();
+    cudaFree(s->flags);
+    s->st_users.release();
+    s->st_ids.release();
+    s->st_scores.release();
+    s->st_count.release();
+    s->st_stats.release();
+    delete s;
+    return GR_OK;
+}
+
+int64_t gr_searcher_launches(const gr_searcher *s) { return s ? s->launches : 0; }
+
+int gr_search_async(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_items *it,
+                    const float *users, int64_t Q, const gr_search_params *p, int64_t *out_ids,
+                    double *out_scores, int32_t *out_count, int64_t *out_stats, void *stream) {
+    if (!s || !g || !m || !it || !users || !out_ids || !out_scores || !out_count || !out_stats)
+        return fail(GR_EINVAL, "null argument");
+    if (int rc = check_params(p)) return rc;
+    if (Q <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(s->device));
+    return launch_search(s, g, m, it, users, Q, p, out_ids, out_scores, out_count, out_stats,
+                         (cudaStream_t)stream);
+}
+
+int gr_searcher_status(gr_searcher *s, void *stream) {
+    if (!s) return fail(GR_EINVAL, "null argument");
+    GR_CUDA(cudaSetDevice(s->device));
+    int flag = 0;
+    GR_CUDA(cudaMemcpyAsync(&flag, s->flags + 1, sizeof(int), cudaMemcpyDeviceToHost,
+                            (cudaStream_t)stream));
+    GR_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
+    if (flag) {
+        GR_CUDA(cudaMemsetAsync(s->flags + 1, 0, sizeof(int), (cudaStream_t)stream));
+        return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
+    }
+    return GR_OK;
+}
+
+int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_items *it,
+              const float *users, int64_t Q, const gr_search_params *p, int64_t *out_ids,
+              double *out_scores, int32_t *out_count, int64_t *out_stats, int on_device,
+              void *stream) {
+    if (!s || !g || !m || !it || !users || !out_ids || !out_scores || !out_count || !out_stats)
+        return fail(GR_EINVAL, "null argument");
+    if (int rc = check_params(p)) return rc;
+    if (Q <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(s->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    GR_CUDA(cudaMemsetAsync(s->flags + 1, 0, sizeof(int), st));
+    const int nst = 5 + g->dg.n_layers;
+    if (on_device) {
+        if (int rc = launch_search(s, g, m, it, users, Q, p, out_ids, out_scores, out_count,
+                                   out_stats, st))
+            return rc;
+    } else {
+        const size_t nu = (size_t)Q * m->dm.d_h, no = (size_t)Q * p->k, ns = (size_t)Q * nst;
+        size_t cap_u = s->st_users_n, cap_s = s->st_stats_n;
+        if (int rc = stage<float>(s->st_users, cap_u, nu)) return rc;
+        s->st_users_n = cap_u;
+        size_t c1 = s->st_out_n, c2 = s->st_out_n, c3 = s->st_out_n;
+        if (no > s->st_out_n || !s->st_ids.p) {
+            s->st_ids.release(); s->st_scores.release(); s->st_count.release();
+            c1 = c2 = c3 = 0;
+            if (int rc = stage<int64_t>(s->st_ids, c1, no)) return rc;
+            if (int rc = stage<double>(s->st_scores, c2, no)) return rc;
+            if (int rc = stage<int32_t>(s->st_count, c3, std::max<size_t>(no, (size_t)Q))) return rc;
+            s->st_out_n = no;
+        }
+        if (int rc = stage<int64_t>(s->st_stats, cap_s, ns)) return rc;
+        s->st_stats_n = cap_s;
+        float *du = (float *)s->st_users.p;
+        GR_CUDA(cudaMemcpyAsync(du, users, nu * 4, cudaMemcpyHostToDevice, st));
+        if (int rc = launch_search(s, g, m, it, du, Q, p, (int64_t *)s->st_ids.p,
+                                   (double *)s->st_scores.p, (int32_t *)s->st_count.p,
+                                   (int64_t *)s->st_stats.p, st))
+            return rc;
+        GR_CUDA(cudaMemcpyAsync(out_ids, s->st_ids.p, no * 8, cudaMemcpyDeviceToHost, st));
+        GR_CUDA(cudaMemcpyAsync(out_scores, s->st_scores.p, no * 8, cudaMemcpyDeviceToHost, st));
+        GR_CUDA(cudaMemcpyAsync(out_count, s->st_count.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, st));
+        GR_CUDA(cudaMemcpyAsync(out_stats, s->st_stats.p, ns * 8, cudaMemcpyDeviceToHost, st));
+    }
+    return gr_searcher_status(s, stream);
+}
+
+// ------------------------------------------------------------------ pairs
+int gr_score_pairs(const gr_model *m, const gr_items *it, const float *users, int64_t n_users,
+                   const int32_t *user_index, const int64_t *item_ids, int64_t n,
+                   double *out_scores, int on_device, void *stream) {
+    if (!m || !it || !users || !item_ids || !out_scores) return fail(GR_EINVAL, "null argument");
+    if (m->dm.d_h != it->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
+    if (n_users < 1) return fail(GR_EINVAL, "no user embeddings");
+    if (n <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    const float *du = users;
+    const int32_t *dui = user_index;
+    const int64_t *dids = item_ids;
+    double *dout = out_scores;
+    std::vector<void *> tmp;
+    auto cleanup = [&](int rc) {
+        for (void *p : tmp) cudaFree(p);
+        return rc;
+    };
+    if (!on_device) {
+        float *a = nullptr;
+        int64_t *b = nullptr;
+        double *c = nullptr;
+        int32_t *u = nullptr;
+        if (int rc = dmalloc(&a, (size_t)n_users * m->dm.d_h)) return cleanup(rc);
+        tmp.push_back(a);
+        if (int rc = dmalloc(&b, (size_t)n)) return cleanup(rc);
+        tmp.push_back(b);
+        if (int rc = dmalloc(&c, (size_t)n)) return cleanup(rc);
+        tmp.push_back(c);
+        cudaMemcpyAsync(a, users, (size_t)n_users * m->dm.d_h * 4, cudaMemcpyHostToDevice, st);
+        cudaMemcpyAsync(b, item_ids, (size_t)n * 8, cudaMemcpyHostToDevice, st);
+        if (user_index) {
+            if (int rc = dmalloc(&u, (size_t)n)) return cleanup(rc);
+            tmp.push_back(u);
+            cudaMemcpyAsync(u, user_index, (size_t)n * 4, cudaMemcpyHostToDevice, st);
+        }
+        du = a;
+        dids = b;
+        dout = c;
+        dui = u;
+    }
+    int *flags = nullptr;
+    if (int rc = dmalloc(&flags, 2)) return cleanup(rc);
+    tmp.push_back(flags);
+    cudaMemsetAsync(flags, 0, 8, st);
+    PairArgs a;
+    std::memset(&a, 0, sizeof(a));
+    const int smem = plan_pairs(m->dm, a);
+    if (int rc = set_smem(score_pairs_kernel, smem)) return cleanup(rc);
+    a.M = m->dm;
+    a.it = it->di;
+    a.users = du;
+    a.n_users = n_users;
+    a.user_index = dui;
+    a.item_ids = dids;
+    a.n = n;
+    a.out = dout;
+    a.nonfinite = flags;
+    a.bad_index = flags + 1;
+    int per_sm = 1;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, score_pairs_kernel, GR_NT, smem);
+    const int64_t tiles = (n + GR_PT - 1) / GR_PT;
+    const int grid = (int)std::min<int64_t>(tiles, (int64_t)std::max(per_sm, 1) * num_sms(m->device));
+    score_pairs_kernel<<<grid, GR_NT, smem, st>>>(a);
+    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(GR_ECUDA, "score_pairs launch failed"));
+    int hflags[2] = {0, 0};
+    cudaMemcpyAsync(hflags, flags, 8, cudaMemcpyDeviceToHost, st);
+    if (!on_device) cudaMemcpyAsync(out_scores, dout, (size_t)n * 8, cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return cleanup(fail(GR_ECUDA, cudaGetErrorString(e)));
+    cleanup(GR_OK);
+    if (hflags[1]) return fail(GR_EINVAL, "user index or item id out of range");
+    if (hflags[0]) return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
+    return GR_OK;
+}
+
+// ------------------------------------------------------------------ brute force
+int gr_brute_force(const gr_model *m, const gr_items *it, const float *users, int64_t Q,
+                   int32_t k, int64_t *out_ids, double *out_scores, int on_device, void *stream) {
+    if (!m || !it || !users || !out_ids || !out_scores) return fail(GR_EINVAL, "null argument");
+    if (m->dm.d_h != it->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
+    if (k < 1 || k > it->di.n) return fail(GR_EINVAL, "k exceeds item count");
+    if (k > 4096) return fail(GR_EINVAL, "k > 4096 not supported");
+    if (Q <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(m->device));
+    cudaStream_t st = (cudaStream_t)stream;
+    BruteArgs a;
+    std::memset(&a, 0, sizeof(a));
+    const int smem = plan_brute(m->dm, a);
+    if (int rc = set_smem(brute_partial_kernel, smem)) return rc;
+    const int sms = num_sms(m->device);
+    const int B = (int)std::min<int64_t>(Q, 16);
+    // partitions per query: fill ~2 CTAs/SM, but keep the merge list (P*k) within 8192 keys
+    const int P = std::max(1, std::min((2 * sms + B - 1) / B, std::max(1, 8192 / k)));
+    a.B = B;
+    a.P = P;
+    a.k = k;
+    a.cap = std::max<int64_t>(4 * k, k + 4096);
+    a.M = m->dm;
+    a.it = it->di;
+    std::vector<void *> tmp;
+    auto cleanup = [&](int rc) {
+        for (void *p : tmp) cudaFree(p);
+        return rc;
+    };
+    float *du = nullptr;
+    int64_t *dids = nullptr;
+    double *dsc = nullptr;
+    if (int rc = dmalloc(&a.cand_key, (size_t)B * P * 2 * a.cap)) return cleanup(rc);
+    tmp.push_back(a.cand_key);
+    if (int rc = dmalloc(&a.cand_row, (size_t)B * P * 2 * a.cap)) return cleanup(rc);
+    tmp.push_back(a.cand_row);
+    if (int rc = dmalloc(&a.loc_key, (size_t)B * P * k)) return cleanup(rc);
+    tmp.push_back(a.loc_key);
+    if (int rc = dmalloc(&a.loc_row, (size_t)B * P * k)) return cleanup(rc);
+    tmp.push_back(a.loc_row);
+    if (int rc = dmalloc(&a.loc_n, (size_t)B * P)) return cleanup(rc);
+    tmp.push_back(a.loc_n);
+    if (int rc = dmalloc(&a.nonfinite, 1)) return cleanup(rc);
+    tmp.push_back(a.nonfinite);
+    cudaMemsetAsync(a.nonfinite, 0, 4, st);
+    if (!on_device) {
+        if (int rc = dmalloc(&du, (size_t)Q * m->dm.d_h)) return cleanup(rc);
+        tmp.push_back(du);
+        if (int rc = dmalloc(&dids, (size_t)Q * k)) return cleanup(rc);
+        tmp.push_back(dids);
+        if (int rc = dmalloc(&dsc, (size_t)Q * k)) return cleanup(rc);
+        tmp.push_back(dsc);
+        cudaMemcpyAsync(du, users, (size_t)Q * m->dm.d_h * 4, cudaMemcpyHostToDevice, st);
+    } else {
+        du = const_cast<float *>(users);
+        dids = out_ids;
+        dsc = out_scores;
+    }
+    const int sortcap = pow2ceil(P * k);
+    const int msmem = sortcap * 12;
+    if (int rc = set_smem(brute_merge_kernel, msmem)) return cleanup(rc);
+    for (int64_t q0 = 0; q0 < Q; q0 += B) {
+        const int nb = (int)std::min<int64_t>(B, Q - q0);
+        a.users = du + q0 * m->dm.d_h;
+        a.B = nb;
+        brute_partial_kernel<<<dim3(P, nb), GR_NT, smem, st>>>(a);
+        brute_merge_kernel<<<nb, GR_NT, msmem, st>>>(a.loc_key, a.loc_row, a.loc_n, P, k, sortcap,
+                                                    dids + q0 * k, dsc + q0 * k);
+    }
+    if (cudaGetLastError() != cudaSuccess) return cleanup(fail(GR_ECUDA, "brute force launch failed"));
+    int flag = 0;
+    cudaMemcpyAsync(&flag, a.nonfinite, 4, cudaMemcpyDeviceToHost, st);
+    if (!on_device) {
+        cudaMemcpyAsync(out_ids, dids, (size_t)Q * k * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out_scores, dsc, (size_t)Q * k * 8, cudaMemcpyDeviceToHost, st);
+    }
+    cudaError_t e = cudaStreamSynchronize(st);
+    cleanup(GR_OK);
+    if (e != cudaSuccess) return fail(GR_ECUDA, cudaGetErrorString(e));
+    if (flag) return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
+    return GR_OK;
+}
+
+// ------------------------------------------------------------------ shard merge
+int gr_merge_topk(int device, const int64_t *in_ids, const double *in_scores, int32_t R, int64_t Q,
+                  int32_t k_in, int32_t k, int64_t *out_ids, double *out_scores,
+                  int32_t *out_count, void *stream) {
+    if (!in_ids || !in_scores || !out_ids || !out_scores || !out_count)
+        return fail(GR_EINVAL, "null argument");
+    if (R < 1 || k_in < 1 || k < 1) return fail(GR_EINVAL, "R, k_in, k must be >= 1");
+    if ((int64_t)R * k_in > 16384) return fail(GR_EINVAL, "R * k_in > 16384 not supported");
+    if (Q <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(device));
+    const int sortcap = pow2ceil(R * k_in);
+    const int smem = sortcap * 12;
+    if (int rc = set_smem(merge_topk_kernel, smem)) return rc;
+    merge_topk_kernel<<<(unsigned)Q, GR_NT, smem, (cudaStream_t)stream>>>(
+        in_ids, in_scores, R, Q, k_in, k, sortcap, out_ids, out_scores, out_count);
+    GR_CUDA(cudaGetLastError());
+    return GR_OK;
+}
+
+} // extern "C"

@@ -1,0 +1,482 @@
+// Persistent hop-synchronous C-HiPANNS kernel (exact-fp32 scoring fused in).
+//
+// One CTA runs one query at a time and pulls the next query index from a global
+// counter (persistent grid = SMs x resident CTAs).  Semantics = the reference
+// c_hipanns in deterministic mode (search.py:194-286) via its hop-synchronous
+// restatement (SURVEY.md §8(a'), pinned by oracle/):
+//
+//   init   claim {entry} + N_top(entry), score them            (search.py:235-236)
+//   layer  seeds = top-kp of everything scored (the pool)      (search.py:239)
+//   hop    expand every searcher's frontier rows; a node goes to the lowest
+//          searcher index listing it (lock-step claim order, search.py:261-265);
+//          score all fresh claims in one dense batch; each searcher keeps the
+//          top-ef of its own claims (search.py:258-259); dead searchers stay dead.
+//
+// Claims use a per-CTA-slot u64 tag array over all slots (epoch-stamped, never
+// cleared): tag = epoch<<32 | (0xFFFFFFFE - searcher) while a hop is claiming
+// (atomicMax keeps the LOWEST searcher index), epoch<<32 | 0xFFFFFFFF once owned.
+// A tag below epoch<<32 means "unclaimed in this query".  One atomic per
+// neighbour read; owners are resolved after a CTA barrier.
+#pragma once
+#include "common.cuh"
+#include "mlp_exact.cuh"
+#include "select.cuh"
+
+struct SearchArgs {
+    DevGraph g;
+    DevModel M;
+    DevItems it;
+    const float *users; // [Q][d_h]
+    int64_t Q;
+    int k, kp, hops, ef;
+    int64_t *out_ids;
+    double *out_scores;
+    int32_t *out_count;
+    int64_t *out_stats;
+    // per-slot scratch
+    uint64_t *tags;    // [slots][n]
+    uint32_t *epochs;  // [slots]
+    int32_t *f_slot;   // [slots][2][capF]
+    int32_t *f_srch;   // [slots][2][capF]
+    int32_t *surv_v;   // [slots][capS]
+    int32_t *surv_i;   // [slots][capS]
+    int32_t *fr_v;     // [slots][capS]
+    int32_t *fr_i;     // [slots][capS]
+    uint64_t *fr_key;  // [slots][capS]
+    int32_t *seg_v;    // [slots][capS]
+    uint64_t *seg_key; // [slots][capS]
+    uint64_t *pool_key; // [slots][2][capP]
+    int32_t *pool_slot; // [slots][2][capP]
+    int64_t capF, capS, capP;
+    int *queue;
+    int *nonfinite;
+    // shared-memory layout (byte offsets into dynamic smem)
+    int off_w0, off_w[GR_MAX_MLP], off_b[GR_MAX_MLP], off_A, off_acc0, off_x0, off_h0, off_h1,
+        off_score, off_hist, off_sortk, off_sortv, off_kp;
+    int ldx0, ldh, sortcap;
+};
+
+struct CtaState {
+    int q;
+    uint32_t epoch;
+    int nF, nS, nFresh, nPool, nPool2, nFn;
+    int pool_cur, f_cur;
+    uint64_t poolT, hopmax, best;
+    int besthop;
+    int64_t per_layer[GR_MAX_LAYERS];
+    int64_t rows, nbrs;
+    uint32_t bcast[4];
+};
+
+__device__ __forceinline__ uint64_t claim_code(uint32_t epoch, int i) {
+    return ((uint64_t)epoch << 32) | (uint64_t)(0xFFFFFFFEu - (uint32_t)i);
+}
+__device__ __forceinline__ uint64_t done_code(uint32_t epoch) {
+    return ((uint64_t)epoch << 32) | 0xFFFFFFFFull;
+}
+
+// warp-aggregated append of (v, i) when ok; returns nothing
+__device__ __forceinline__ void warp_append2(bool ok, int32_t v, int32_t i, int *counter,
+                                             int32_t *dv, int32_t *di) {
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = __ballot_sync(0xffffffffu, ok);
+    if (!mask) return;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(counter, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ok) {
+        const int pos = base + __popc(mask & ((1u << lane) - 1u));
+        dv[pos] = v;
+        di[pos] = i;
+    }
+}
+
+template <int MINB>
+__global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const SearchArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ CtaState st;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const DevModel &M = a.M;
+    const DevGraph &g = a.g;
+
+    // ---- carve shared memory, load weights once per CTA
+    float4 *sW0 = reinterpret_cast<float4 *>(smem + a.off_w0);
+    const float4 *sWm[GR_MAX_MLP];
+    const float *sbm[GR_MAX_MLP];
+    const int O0 = M.dims[1], K0 = M.dims[0], nch0 = M.nch[0], pre = M.pre_ch;
+    {
+        const int n0 = (nch0 - pre) * O0;
+        for (int t = tid; t < n0; t += GR_NT) sW0[t] = M.W[0][pre * O0 + t];
+        for (int m = 0; m < M.n_mlp; ++m) {
+            float *sb = reinterpret_cast<float *>(smem + a.off_b[m]);
+            for (int t = tid; t < M.dims[m + 1]; t += GR_NT) sb[t] = M.b[m][t];
+            sbm[m] = sb;
+            if (m >= 1) {
+                float4 *sw = reinterpret_cast<float4 *>(smem + a.off_w[m]);
+                const int nw = M.nch[m] * M.dims[m + 1];
+                for (int t = tid; t < nw; t += GR_NT) sw[t] = M.W[m][t];
+                sWm[m] = sw;
+            } else {
+                sWm[0] = sW0;
+            }
+        }
+        float4 *sA = reinterpret_cast<float4 *>(smem + a.off_A);
+        for (int t = tid; t < M.nch[M.n_mlp]; t += GR_NT) sA[t] = M.A[t];
+    }
+    const float4 *sA = reinterpret_cast<const float4 *>(smem + a.off_A);
+    float4 *sAcc0 = reinterpret_cast<float4 *>(smem + a.off_acc0);
+    TileSmem S;
+    S.x0 = reinterpret_cast<float4 *>(smem + a.off_x0);
+    S.ldx0 = a.ldx0;
+    S.h[0] = reinterpret_cast<float4 *>(smem + a.off_h0);
+    S.h[1] = reinterpret_cast<float4 *>(smem + a.off_h1);
+    S.ldh = a.ldh;
+    S.score = reinterpret_cast<float *>(smem + a.off_score);
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem + a.off_hist); // [GR_NW][256]
+    uint64_t *sortk = reinterpret_cast<uint64_t *>(smem + a.off_sortk);
+    int32_t *sortv = reinterpret_cast<int32_t *>(smem + a.off_sortv);
+    int32_t *seg_cnt = reinterpret_cast<int32_t *>(smem + a.off_kp);
+    int32_t *seg_off = seg_cnt + a.kp;
+    int32_t *fn_off = seg_off + a.kp;
+    const int x0_nch = nch0 - pre;
+    // zero activation buffers once (padding lanes stay zero)
+    for (int t = tid; t < GR_PT * a.ldx0; t += GR_NT) S.x0[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int t = tid; t < GR_PT * a.ldh; t += GR_NT) {
+        S.h[0][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        S.h[1][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+
+    // ---- per-slot scratch
+    const int64_t slot = blockIdx.x;
+    uint64_t *tags = a.tags + slot * g.n;
+    int32_t *fslot[2] = {a.f_slot + slot * 2 * a.capF, a.f_slot + slot * 2 * a.capF + a.capF};
+    int32_t *fsrch[2] = {a.f_srch + slot * 2 * a.capF, a.f_srch + slot * 2 * a.capF + a.capF};
+    int32_t *surv_v = a.surv_v + slot * a.capS, *surv_i = a.surv_i + slot * a.capS;
+    int32_t *fr_v = a.fr_v + slot * a.capS, *fr_i = a.fr_i + slot * a.capS;
+    uint64_t *fr_key = a.fr_key + slot * a.capS;
+    int32_t *seg_v = a.seg_v + slot * a.capS;
+    uint64_t *seg_key = a.seg_key + slot * a.capS;
+    uint64_t *pkey[2] = {a.pool_key + slot * 2 * a.capP, a.pool_key + slot * 2 * a.capP + a.capP};
+    int32_t *pslot[2] = {a.pool_slot + slot * 2 * a.capP, a.pool_slot + slot * 2 * a.capP + a.capP};
+    const int d_h = M.d_h;
+    const bool fast_fill = (d_h % 16) == 0;
+    const int top = g.n_layers - 1;
+    const int nst = 5 + g.n_layers;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) {
+            st.q = atomicAdd(a.queue, 1);
+            if (st.q < a.Q) {
+                const uint32_t e = a.epochs[slot] + 1u;
+                a.epochs[slot] = e;
+                st.epoch = e;
+            }
+            st.nPool = 0; st.pool_cur = 0; st.f_cur = 0; st.poolT = 0ull;
+            st.hopmax = 0ull; st.best = 0ull; st.besthop = -1;
+            for (int l = 0; l < GR_MAX_LAYERS; ++l) st.per_layer[l] = 0;
+            st.rows = 0; st.nbrs = 0;
+        }
+        __syncthreads();
+        const int64_t q = st.q;
+        if (q >= a.Q) break;
+        const uint32_t epoch = st.epoch;
+        const float *hu = a.users + q * d_h;
+
+        // ---- hoisted user-half accumulators of layer 0
+        for (int o = tid; o < O0; o += GR_NT) {
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int j = 0; j < pre; ++j) {
+                const int c = chunk_perm(j, K0);
+                const float4 x = make_float4(hu[4 * c], hu[4 * c + 1], hu[4 * c + 2], hu[4 * c + 3]);
+                mac4(acc, x, M.W[0][j * O0 + o]);
+            }
+            sAcc0[o] = acc;
+        }
+
+        // ---- score fr_v[0..nFresh) (hop h, layer L): keys, pool append, hop max
+        auto score_fresh = [&](int nFresh) {
+            const int pc = st.pool_cur;
+            const uint64_t poolT = st.poolT;
+            for (int base = 0; base < nFresh; base += GR_PT) {
+                const int nv = min(GR_PT, nFresh - base);
+                // gather item rows into x0 (processing order)
+                for (int pp = 0; pp < 4; ++pp) {
+                    const int p = warp * 4 + pp;
+                    float4 *xr = S.x0 + p * a.ldx0;
+                    if (p < nv) {
+                        const int32_t s = fr_v[base + p];
+                        const float *hv = a.it.emb + slot_row(g, s) * a.it.ld;
+                        if (fast_fill) {
+                            for (int cc = lane; cc < d_h / 4; cc += 32) {
+                                const float4 v = __ldg(reinterpret_cast<const float4 *>(hv) + cc);
+                                xr[chunk_perm(d_h / 4 + cc, K0) - pre] = v;
+                            }
+                        } else {
+                            for (int jj = lane; jj < x0_nch; jj += 32) {
+                                const int c = chunk_perm(pre + jj, K0);
+                                float e[4];
+#pragma unroll
+                                for (int u = 0; u < 4; ++u) {
+                                    const int idx = 4 * c + u;
+                                    e[u] = idx < d_h ? hu[idx] : (idx < 2 * d_h ? hv[idx - d_h] : 0.f);
+                                }
+                                xr[jj] = make_float4(e[0], e[1], e[2], e[3]);
+                            }
+                        }
+                    } else {
+                        for (int jj = lane; jj < x0_nch; jj += 32) xr[jj] = make_float4(0.f, 0.f, 0.f, 0.f);
+                    }
+                }
+                __syncthreads();
+                mlp_tile(M, S, sWm, sbm, sA, sW0, x0_nch, pre > 0 ? sAcc0 : nullptr, nv, a.nonfinite);
+                __syncthreads();
+                if (tid < nv) {
+                    const int32_t s = fr_v[base + tid];
+                    const uint64_t key = make_key(S.score[tid], slot_rank(g, s));
+                    fr_key[base + tid] = key;
+                    atomicMax(reinterpret_cast<unsigned long long *>(&st.hopmax), key);
+                    if (key > poolT) {
+                        const int idx = atomicAdd(&st.nPool, 1);
+                        pkey[pc][idx] = key;
+                        pslot[pc][idx] = s;
+                    }
+                }
+            }
+            __syncthreads();
+        };
+
+        // ---- after scoring: best tracking, per-layer count, pool compaction to top-k
+        auto after_score = [&](int layer, int h, int nFresh) {
+            if (tid == 0) {
+                st.per_layer[layer] += nFresh;
+                if (st.hopmax > st.best) { st.best = st.hopmax; st.besthop = h; }
+                st.hopmax = 0ull;
+            }
+            __syncthreads();
+            if (st.nPool > a.k) {
+                const int pc = st.pool_cur;
+                const uint64_t T = cta_select_threshold(pkey[pc], st.nPool, a.k, hist, st.bcast);
+                if (tid == 0) st.nPool2 = 0;
+                __syncthreads();
+                const int np = st.nPool;
+                for (int i = tid; i < np; i += GR_NT) {
+                    const uint64_t key = pkey[pc][i];
+                    if (key >= T) {
+                        const int idx = atomicAdd(&st.nPool2, 1);
+                        pkey[pc ^ 1][idx] = key;
+                        pslot[pc ^ 1][idx] = pslot[pc][i];
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) { st.pool_cur = pc ^ 1; st.nPool = st.nPool2; st.poolT = T; }
+                __syncthreads();
+            }
+        };
+
+        // ---- owner resolution: survivors whose tag still carries their code own the node
+        auto resolve = [&](int nS, int fresh_base) {
+            const uint64_t done = done_code(epoch);
+            for (int t0 = 0; t0 < nS; t0 += GR_NT) {
+                const int t = t0 + tid;
+                bool ok = false;
+                int32_t v = 0, i = 0;
+                if (t < nS) {
+                    v = surv_v[t];
+                    i = surv_i[t];
+                    // L2 read: the tag was last written by atomics (performed at L2)
+                    if (__ldcg(reinterpret_cast<const unsigned long long *>(tags + v)) ==
+                        claim_code(epoch, i))
+                        ok = true;
+                }
+                __syncwarp();
+                warp_append2(ok, v, i, &st.nFresh, fr_v, fr_i);
+                (void)fresh_base;
+            }
+            __syncthreads();
+            // owners mark done (after everyone compared against the claim codes)
+            const int nF = st.nFresh;
+            for (int t = tid; t < nF; t += GR_NT) tags[fr_v[t]] = done;
+            __syncthreads();
+        };
+
+        // ================= init: entry + its top-layer neighbourhood (hop 0)
+        if (tid == 0) {
+            tags[g.entry] = done_code(epoch);
+            fr_v[0] = g.entry;
+            fr_i[0] = 0;
+            st.nFresh = 1;
+            st.nS = 0;
+        }
+        __syncthreads();
+        if (warp == 0) {
+            const int32_t *row = graph_row(g, top, g.entry);
+            if (lane == 0) st.rows += 1;
+            if (row) {
+                const uint64_t code = claim_code(epoch, 0);
+                for (int c0 = 0; c0 < g.deg[top]; c0 += 32) {
+                    const int32_t v = (c0 + lane < g.deg[top]) ? __ldg(row + c0 + lane) : -1;
+                    const unsigned nv = __popc(__ballot_sync(0xffffffffu, v >= 0));
+                    if (lane == 0) st.nbrs += nv;
+                    bool ok = false;
+                    if (v >= 0) {
+                        const uint64_t old = atomicMax(reinterpret_cast<unsigned long long *>(tags + v), code);
+                        ok = old < code;
+                    }
+                    warp_append2(ok, v, 0, &st.nS, surv_v, surv_i);
+                }
+            }
+        }
+        __syncthreads();
+        resolve(st.nS, 1);
+        {
+            const int nFresh = st.nFresh;
+            score_fresh(nFresh);
+            after_score(top, 0, nFresh);
+        }
+
+        int h = 0;
+        for (int layer = top; layer >= 0; --layer) {
+            // ---- seeds: sorted pool, first min(kp, |pool|)
+            {
+                const int np = st.nPool, pc = st.pool_cur;
+                for (int i = tid; i < np; i += GR_NT) { sortk[i] = pkey[pc][i]; sortv[i] = pslot[pc][i]; }
+                __syncthreads();
+                cta_sort_desc(sortk, sortv, np, a.sortcap);
+                const int ns = min(a.kp, np);
+                for (int i = tid; i < ns; i += GR_NT) { fslot[0][i] = sortv[i]; fsrch[0][i] = i; }
+                if (tid == 0) { st.nF = ns; st.f_cur = 0; }
+                __syncthreads();
+            }
+            const int deg = g.deg[layer];
+            for (int t = 0; t < a.hops; ++t) {
+                ++h;
+                const int nF = st.nF;
+                if (nF == 0) { h += a.hops - 1 - t; break; }
+                const int fc = st.f_cur;
+                if (tid == 0) { st.nS = 0; st.nFresh = 0; }
+                __syncthreads();
+                // ---- expand + claim (4 frontier rows in flight per warp)
+                for (int e0 = warp * 4; e0 < nF; e0 += GR_NW * 4) {
+                    int32_t s[4], srch[4];
+                    const int32_t *row[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u;
+                        s[u] = e < nF ? fslot[fc][e] : -1;
+                        srch[u] = e < nF ? fsrch[fc][e] : 0;
+                        row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
+                    }
+                    int nvalid = 0;
+                    for (int c0 = 0; c0 < deg; c0 += 32) {
+                        int32_t v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            v[u] = (row[u] && c0 + lane < deg) ? __ldg(row[u] + c0 + lane) : -1;
+                            nvalid += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            bool ok = false;
+                            if (v[u] >= 0) {
+                                const uint64_t code = claim_code(epoch, srch[u]);
+                                const uint64_t old =
+                                    atomicMax(reinterpret_cast<unsigned long long *>(tags + v[u]), code);
+                                ok = old < code;
+                            }
+                            warp_append2(ok, v[u], srch[u], &st.nS, surv_v, surv_i);
+                        }
+                    }
+                    if (lane == 0) {
+                        atomicAdd(reinterpret_cast<unsigned long long *>(&st.nbrs), (unsigned long long)nvalid);
+                        atomicAdd(reinterpret_cast<unsigned long long *>(&st.rows),
+                                  (unsigned long long)min(4, nF - e0));
+                    }
+                }
+                __syncthreads();
+                resolve(st.nS, 0);
+                const int nFresh = st.nFresh;
+                score_fresh(nFresh);
+                after_score(layer, h, nFresh);
+                if (t == a.hops - 1) break; // frontier after a layer's last hop is unused
+                // ---- per-searcher top-ef of fresh claims -> next frontier
+                const int nsr = a.kp;
+                for (int i = tid; i < nsr; i += GR_NT) seg_cnt[i] = 0;
+                __syncthreads();
+                for (int t2 = tid; t2 < nFresh; t2 += GR_NT) atomicAdd(&seg_cnt[fr_i[t2]], 1);
+                __syncthreads();
+                if (tid == 0) {
+                    int acc = 0, accf = 0;
+                    for (int i = 0; i < nsr; ++i) {
+                        seg_off[i] = acc;
+                        fn_off[i] = accf;
+                        acc += seg_cnt[i];
+                        accf += min(seg_cnt[i], a.ef);
+                        seg_cnt[i] = 0; // reused as scatter cursor
+                    }
+                    st.nFn = accf;
+                }
+                __syncthreads();
+                for (int t2 = tid; t2 < nFresh; t2 += GR_NT) {
+                    const int i = fr_i[t2];
+                    const int pos = seg_off[i] + atomicAdd(&seg_cnt[i], 1);
+                    seg_v[pos] = fr_v[t2];
+                    seg_key[pos] = fr_key[t2];
+                }
+                __syncthreads();
+                const int fn = fc ^ 1;
+                for (int i = warp; i < nsr; i += GR_NW) {
+                    const int ni = seg_cnt[i], off = seg_off[i], fo = fn_off[i];
+                    if (ni <= a.ef) {
+                        for (int j = lane; j < ni; j += 32) { fslot[fn][fo + j] = seg_v[off + j]; fsrch[fn][fo + j] = i; }
+                    } else {
+                        const uint64_t T = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
+                        int cnt = 0;
+                        for (int j0 = 0; j0 < ni; j0 += 32) {
+                            const int j = j0 + lane;
+                            const bool keep = j < ni && seg_key[off + j] >= T;
+                            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                            if (keep) {
+                                const int pos = fo + cnt + __popc(mask & ((1u << lane) - 1u));
+                                fslot[fn][pos] = seg_v[off + j];
+                                fsrch[fn][pos] = i;
+                            }
+                            cnt += __popc(mask);
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) { st.nF = st.nFn; st.f_cur = fn; }
+                __syncthreads();
+            }
+        }
+
+        // ---- result: pool sorted (score desc, id asc), first min(k, |pool|)
+        {
+            const int np = st.nPool, pc = st.pool_cur;
+            for (int i = tid; i < np; i += GR_NT) { sortk[i] = pkey[pc][i]; sortv[i] = pslot[pc][i]; }
+            __syncthreads();
+            cta_sort_desc(sortk, sortv, np, a.sortcap);
+            const int nr = min(a.k, np);
+            for (int j = tid; j < a.k; j += GR_NT) {
+                if (j < nr) {
+                    a.out_ids[q * a.k + j] = g.ids[sortv[j]];
+                    a.out_scores[q * a.k + j] = (double)orderable_f32((uint32_t)(sortk[j] >> 32));
+                } else {
+                    a.out_ids[q * a.k + j] = -1;
+                    a.out_scores[q * a.k + j] = __longlong_as_double(0x7ff8000000000000ll);
+                }
+            }
+            if (tid == 0) {
+                a.out_count[q] = nr;
+                int64_t ev = 0;
+                for (int l = 0; l < g.n_layers; ++l) { ev += st.per_layer[l]; a.out_stats[q * nst + 5 + l] = st.per_layer[l]; }
+                a.out_stats[q * nst + 0] = ev;
+                a.out_stats[q * nst + 1] = ev;
+                a.out_stats[q * nst + 2] = nr > 0 ? st.besthop : -1;
+                a.out_stats[q * nst + 3] = st.rows;
+                a.out_stats[q * nst + 4] = st.nbrs;
+            }
+        }
+    }
+}

@@ -1,0 +1,73 @@
+"""Synthetic workloads of the BASELINE.json shapes (bench.py, scaling runs).
+
+Same recipe as the reference's benchmark inputs: clustered item
+features (``nann.bench.clustered_vectors``: centres N(0, 4^2), unit noise,
+bench.py:24-28) projected by ``create_model(d, d, Z, (64, 64), seed=1)``'s item tower,
+user embeddings from the user tower over N(0, 1) features, graph over the item
+embeddings with degree cap 2m.  At 10M items the generation runs on the GPU with
+torch (seeded) — identical bytes on every rank — instead of numpy.
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass
+
+import numpy as np
+
+from .index import GraphIndex
+from .metric import RelevanceModel, create_model
+
+CONFIGS = {
+    # name: (n_items, d, m, n_clusters, Z, queries per GPU)
+    "cfg1": (100_000, 64, 16, 256, 2, 1_000),
+    "cfg2": (1_000_000, 128, 16, 1024, 3, 10_000),
+    "cfg3": (10_000_000, 128, 24, 4096, 3, 65_536),
+    "small": (200_000, 128, 24, 512, 3, 8_192),
+}
+
+
+@dataclass
+class Workload:
+    name: str
+    model: RelevanceModel
+    items: "object"        # torch fp32 [N, d] on the device
+    items_host: np.ndarray | None
+    users: np.ndarray      # fp32 [Q, d] (host)
+    index: GraphIndex
+    build_s: float
+
+
+def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
+         n_queries: int | None = None, n_items: int | None = None) -> Workload:
+    import torch
+
+    N, d, m, C, Z, Q = CONFIGS[name]
+    N = n_items or N
+    Q = n_queries or Q
+    t0 = time.perf_counter()
+    dev = torch.device("cuda", device)
+    model = create_model(d_x=d, d_h=d, z_dim=Z, hidden=(64, 64), seed=1)
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    centers = torch.randn(C, d, generator=g, device=dev) * 4.0
+    assign = torch.randint(0, C, (N,), generator=g, device=dev)
+    w_item = torch.from_numpy(model.item_projector.weight.astype(np.float32)).to(dev)
+    items = torch.empty((N, d), dtype=torch.float32, device=dev)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    for s in range(0, N, 1 << 20):
+        e = min(N, s + (1 << 20))
+        feats = centers[assign[s:e]] + torch.randn(e - s, d, generator=g, device=dev)
+        items[s:e] = feats @ w_item
+    gu = torch.Generator(device=dev)
+    gu.manual_seed(7 + 1000 * rank)
+    w_user = torch.from_numpy(model.user_projector.weight.astype(np.float32)).to(dev)
+    users = (torch.randn(Q, d, generator=gu, device=dev) @ w_user).cpu().numpy()
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    del centers, assign
+    index = GraphIndex.build(items, m=m, seed=0, device=dev)
+    torch.cuda.synchronize(dev)
+    items_host = items.cpu().numpy() if host_items else None
+    return Workload(name, model, items, items_host, np.ascontiguousarray(users, np.float32), index,
+                    time.perf_counter() - t0)

@@ -66,6 +66,41 @@ def model_arrays(model, prefix="") -> dict:
     return out
 
 
+class WorkCounter:
+    """Counts _neighbors_of calls / ids per query (SURVEY.md Appendix A count_work.py)."""
+
+    def __init__(self):
+        import nann.search as S
+        self.S = S
+        self.orig = S._neighbors_of
+        self.rows = 0
+        self.ids = 0
+
+        def wrapped(layers, layer, slot):
+            out = self.orig(layers, layer, slot)
+            self.rows += 1
+            self.ids += len(out)
+            return out
+
+        S._neighbors_of = wrapped
+
+    def take(self):
+        r = (self.rows, self.ids)
+        self.rows = self.ids = 0
+        return r
+
+
+COUNTER = None
+
+
+def run_counted(fn):
+    """Run one c_hipanns call; returns (result, rows_expanded, neighbour_ids_read)."""
+    COUNTER.take()
+    r = fn()
+    rows, ids = COUNTER.take()
+    return r, rows, ids
+
+
 def result_arrays(results, k) -> dict:
     Q = len(results)
     ids = np.full((Q, k), -1, dtype=np.int64)
@@ -75,7 +110,11 @@ def result_arrays(results, k) -> dict:
     visited = np.zeros(Q, dtype=np.int64)
     best_hop = np.full(Q, -1, dtype=np.int64)
     per_layer = []
-    for q, r in enumerate(results):
+    rows = np.zeros(Q, dtype=np.int64)
+    nbr = np.zeros(Q, dtype=np.int64)
+    for q, (r, nr, ni) in enumerate(results):
+        rows[q] = nr
+        nbr[q] = ni
         n_items[q] = len(r.items)
         for j, (i, s) in enumerate(r.items):
             ids[q, j] = i
@@ -85,7 +124,7 @@ def result_arrays(results, k) -> dict:
         best_hop[q] = -1 if r.stats.hops_to_best is None else r.stats.hops_to_best
         per_layer.append(r.stats.per_layer_evaluations)
     return {"res_ids": ids, "res_scores": scores, "res_n": n_items, "res_evals": evals,
-            "res_visited": visited, "res_best_hop": best_hop,
+            "res_visited": visited, "res_best_hop": best_hop, "res_rows": rows, "res_nbr_ids": nbr,
             "res_per_layer": np.asarray(per_layer, dtype=np.int64)}
 
 
@@ -152,7 +191,8 @@ def search_fixture(name, n, d, z, m, n_clusters, n_queries, params, shuffle_ids=
     out.update(model_arrays(model))
     for pi, p in enumerate(params):
         sp = SearchParams(**p)
-        res = [c_hipanns(index, model_scorer(model, users[q], emb), sp) for q in range(n_queries)]
+        res = [run_counted(lambda q=q: c_hipanns(index, model_scorer(model, users[q], emb), sp))
+               for q in range(n_queries)]
         for key, val in result_arrays(res, sp.k).items():
             out[f"p{pi}/{key}"] = val
         out[f"p{pi}/params"] = np.array([sp.k, sp.k_parallel, sp.hops, sp.frontier_width])
@@ -179,7 +219,8 @@ def euclid_fixture():
     out.update(graph_arrays(index))
     for pi, p in enumerate(PARAMS[1:] + [dict(k=10, k_parallel=4, hops=3)]):
         sp = SearchParams(**p)
-        res = [c_hipanns(index, euclidean_scorer(queries[q], vectors), sp) for q in range(16)]
+        res = [run_counted(lambda q=q: c_hipanns(index, euclidean_scorer(queries[q], vectors), sp))
+               for q in range(16)]
         for key, val in result_arrays(res, sp.k).items():
             out[f"p{pi}/{key}"] = val
         out[f"p{pi}/params"] = np.array([sp.k, sp.k_parallel, sp.hops, sp.frontier_width])
@@ -187,7 +228,9 @@ def euclid_fixture():
 
 
 def main():
+    global COUNTER
     print("reference nann", nann.__version__, "from", nann.__file__)
+    COUNTER = WorkCounter()
     scorer_fixture()
     euclid_fixture()
     search_fixture("search_d64_z2", n=3000, d=64, z=2, m=8, n_clusters=32, n_queries=24,

@@ -40,7 +40,8 @@ def param_sets(z):
 def expected(z, pi):
     p = f"p{pi}/"
     return {key: z[p + "res_" + key] for key in
-            ("ids", "scores", "n", "evals", "visited", "best_hop", "per_layer")}
+            ("ids", "scores", "n", "evals", "visited", "best_hop", "per_layer", "rows",
+                         "nbr_ids")}
 
 
 SEARCH_FIXTURES = ["search_d64_z2", "search_d128_z3", "search_d32_shuffled"]

@@ -107,3 +107,5 @@ def test_c_oracle_search_matches_reference(fixture):
         np.testing.assert_array_equal(r["visited"], exp["visited"])
         np.testing.assert_array_equal(r["best_hop"], exp["best_hop"])
         np.testing.assert_array_equal(r["per_layer"], exp["per_layer"])
+        np.testing.assert_array_equal(r["rows"], exp["rows"])
+        np.testing.assert_array_equal(r["nbr_ids"], exp["nbr_ids"])
