@@ -179,8 +179,53 @@ def symmetric_prune(idx, dd, cap: int):
     return rows, deg.to(torch.int32)
 
 
+def long_links(x, n_links: int, seed: int, scales=(64, 1024)):
+    """Navigability links (the role HNSW's early insertions play): every node links to its
+    nearest members of sparse random samples of the layer (1/64, 1/1024 of it), so clusters
+    that a k-NN graph leaves disconnected get bridged at several length scales."""
+    torch = _torch()
+    M, dev = x.shape[0], x.device
+    g = torch.Generator(device=dev)
+    g.manual_seed(seed + 7919)
+    per = max(1, n_links // len(scales))
+    idx_parts, d_parts = [], []
+    for sc in scales:
+        S = max(per + 1, M // sc)
+        if S >= M:
+            continue
+        samp = torch.randperm(M, generator=g, device=dev)[:S]
+        near = _assign(x, x[samp], per + 1)           # nearest sample points
+        cand = samp[near]                               # [M, per+1]
+        cand = torch.where(cand == torch.arange(M, device=dev)[:, None], -1, cand)
+        d2 = ((x[:, None, :] - x[cand.clamp_min(0)]) ** 2).sum(-1)
+        d2 = torch.where(cand < 0, float("inf"), d2)
+        idx_parts.append(cand)
+        d_parts.append(d2)
+    if not idx_parts:
+        return None
+    return torch.cat(idx_parts, 1), torch.cat(d_parts, 1)
+
+
+def merge_rows(r1, c1, r2, c2, cap: int):
+    """Union of two symmetric row sets (degree caps add up to <= cap), duplicates dropped."""
+    torch = _torch()
+    M = r1.shape[0]
+    both = torch.cat([r1, r2], 1).long()
+    valid = torch.cat([torch.arange(r1.shape[1], device=r1.device)[None, :] < c1[:, None],
+                       torch.arange(r2.shape[1], device=r1.device)[None, :] < c2[:, None]], 1)
+    both = torch.where(valid, both, torch.full_like(both, M))
+    both, _ = torch.sort(both, 1)
+    dup = torch.zeros_like(valid)
+    dup[:, 1:] = both[:, 1:] == both[:, :-1]
+    both = torch.where(dup, torch.full_like(both, M), both)
+    both, _ = torch.sort(both, 1)
+    cnt = (both < M).sum(1)
+    rows = torch.where(both < M, both, torch.full_like(both, -1))[:, :cap].to(torch.int32)
+    return rows, cnt.to(torch.int32)
+
+
 def build_layers(vectors, m: int = 16, level_prob: float = 1.0 / 17.0, max_layers: int = 4,
-                 seed: int = 0, device=None, exact_limit: int = 200_000):
+                 seed: int = 0, device=None, exact_limit: int = 200_000, long_frac: float = 0.0):
     """Return dict(levels, entry_slot, n_layers, nbrs=[(n, cap_l) int32], cnts=[(n,) int32])."""
     torch = _torch()
     dev = torch.device(device if device is not None else "cuda")
@@ -206,7 +251,12 @@ def build_layers(vectors, m: int = 16, level_prob: float = 1.0 / 17.0, max_layer
                 idx, dd = knn_exact(xm, K)
             else:
                 idx, dd = knn_ivf(xm, K, seed=seed + l)
-            r, c = symmetric_prune(idx, dd, cap)
+            c_long = int(cap * long_frac) if M > 4 * cap else 0
+            r, c = symmetric_prune(idx, dd, cap - c_long)
+            ll = long_links(xm, c_long, seed + 31 * l) if c_long else None
+            if ll is not None:
+                rl, cl = symmetric_prune(ll[0], ll[1], c_long)
+                r, c = merge_rows(r, c, rl, cl, cap)
             glob = torch.where(r >= 0, mem[r.clamp_min(0).long()].to(torch.int32),
                                torch.zeros_like(r))
             mem_h = mem.cpu().numpy()

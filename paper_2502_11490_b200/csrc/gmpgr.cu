@@ -393,18 +393,55 @@ int hidden_ld(const DevModel &M) {
     return odd(mx);
 }
 
-int plan_search(const DevModel &M, int k, int kp, SearchArgs &a) {
+// which compile-time scorer fits this model (0: generic)
+int fixed_shape(const DevModel &M) {
+    if (M.n_mlp != 3 || !M.relu || M.dims[1] != 64 || M.dims[2] != 64) return 0;
+    const int dh = M.d_h, z = M.Z;
+    if ((dh == 128 || dh == 64) && (z == 2 || z == 3)) return dh * 10 + z;
+    return 0;
+}
+
+template <int DH, int ZZ>
+void plan_fixed(SearchArgs &a) {
+    using F = FixedMlp<DH, ZZ>;
+    a.off_w0 = F::OFF_W0 * 16;
+    a.off_w[0] = 0;
+    a.off_w[1] = F::OFF_W1 * 16;
+    a.off_w[2] = F::OFF_W2 * 16;
+    a.off_b[0] = F::OFF_B0 * 16;
+    a.off_b[1] = F::OFF_B1 * 16;
+    a.off_b[2] = F::OFF_B2 * 16;
+    a.off_A = F::OFF_A * 16;
+    a.off_acc0 = F::OFF_ACC0 * 16;
+    a.off_x0 = F::OFF_X0 * 16;
+    a.ldx0 = F::LDX0;
+    a.off_h0 = F::OFF_H0 * 16;
+    a.off_h1 = F::OFF_H1 * 16;
+    a.ldh = F::LDH;
+    a.off_score = F::OFF_SCORE * 16;
+}
+
+int plan_search(const DevModel &M, int k, int kp, SearchArgs &a, int shape) {
     SmemPlan P;
-    const int x0_nch = M.nch[0] - M.pre_ch;
-    a.off_w0 = P.alloc(x0_nch * M.dims[1] * 16);
-    plan_weights(M, P, a.off_w, a.off_b, &a.off_A);
-    a.off_acc0 = P.alloc(M.dims[1] * 16);
-    a.ldx0 = odd(x0_nch);
-    a.off_x0 = P.alloc(GR_PT * a.ldx0 * 16);
-    a.ldh = hidden_ld(M);
-    a.off_h0 = P.alloc(GR_PT * a.ldh * 16);
-    a.off_h1 = P.alloc(GR_PT * a.ldh * 16);
-    a.off_score = P.alloc(GR_PT * 4);
+    if (shape) {
+        switch (shape) {
+        case 1283: plan_fixed<128, 3>(a); P.bytes = FixedMlp<128, 3>::TOTAL * 16; break;
+        case 1282: plan_fixed<128, 2>(a); P.bytes = FixedMlp<128, 2>::TOTAL * 16; break;
+        case 643: plan_fixed<64, 3>(a); P.bytes = FixedMlp<64, 3>::TOTAL * 16; break;
+        default: plan_fixed<64, 2>(a); P.bytes = FixedMlp<64, 2>::TOTAL * 16; break;
+        }
+    } else {
+        const int x0_nch = M.nch[0] - M.pre_ch;
+        a.off_w0 = P.alloc(x0_nch * M.dims[1] * 16);
+        plan_weights(M, P, a.off_w, a.off_b, &a.off_A);
+        a.off_acc0 = P.alloc(M.dims[1] * 16);
+        a.ldx0 = odd(x0_nch);
+        a.off_x0 = P.alloc(GR_PT * a.ldx0 * 16);
+        a.ldh = hidden_ld(M);
+        a.off_h0 = P.alloc(GR_PT * a.ldh * 16);
+        a.off_h1 = P.alloc(GR_PT * a.ldh * 16);
+        a.off_score = P.alloc(GR_PT * 4);
+    }
     a.off_hist = P.alloc(GR_NW * 256 * 4);
     a.sortcap = pow2ceil(std::max(k, kp));
     a.off_sortk = P.alloc(a.sortcap * 8);
@@ -516,16 +553,20 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     if (M->dm.d_h != I->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
-    const int smem = plan_search(M->dm, p->k, p->k_parallel, a);
-    const bool two = smem <= 110 * 1024;
-    if (two) {
-        if (int rc = set_smem(hipanns_search_kernel<2>, smem)) return rc;
-    } else {
-        if (int rc = set_smem(hipanns_search_kernel<1>, smem)) return rc;
+    const int shape = fixed_shape(M->dm);
+    const int smem = plan_search(M->dm, p->k, p->k_parallel, a, shape);
+    void (*kern)(const SearchArgs) = nullptr;
+    switch (shape) {
+    case 1283: kern = hipanns_search_kernel<2, 128, 3>; break;
+    case 1282: kern = hipanns_search_kernel<2, 128, 2>; break;
+    case 643: kern = hipanns_search_kernel<2, 64, 3>; break;
+    case 642: kern = hipanns_search_kernel<2, 64, 2>; break;
+    default:
+        kern = smem <= 110 * 1024 ? hipanns_search_kernel<2, 0, 0> : hipanns_search_kernel<1, 0, 0>;
     }
+    if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 0;
-    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(
-        &per_sm, two ? hipanns_search_kernel<2> : hipanns_search_kernel<1>, GR_NT, smem));
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GR_NT, smem));
     if (per_sm < 1) return fail(GR_EINVAL, "search kernel does not fit on an SM");
     int64_t slots = std::min<int64_t>(Q, (int64_t)per_sm * num_sms(G->device));
     const int64_t capF = (int64_t)p->k_parallel * p->ef;
@@ -565,10 +606,7 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     a.queue = S->flags;
     a.nonfinite = S->flags + 1;
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
-    if (two)
-        hipanns_search_kernel<2><<<(int)slots, GR_NT, smem, stream>>>(a);
-    else
-        hipanns_search_kernel<1><<<(int)slots, GR_NT, smem, stream>>>(a);
+    kern<<<(int)slots, GR_NT, smem, stream>>>(a);
     GR_CUDA(cudaGetLastError());
     S->launches += 1;
     return GR_OK;

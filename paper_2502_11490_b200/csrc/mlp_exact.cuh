@@ -134,3 +134,117 @@ __device__ __forceinline__ void mlp_tile(const DevModel &M, const TileSmem &S,
     }
     (void)Z;
 }
+
+// ---------------------------------------------------------------------------
+// Compile-time-shaped variant for the BASELINE model family
+// (create_model(d, d, Z, hidden=(64, 64)), metric.py:229-267; evalharness.py:77):
+// d_h = D_H (multiple of 16, user half hoisted), H0 = H1 = 64, Z outputs.  All smem
+// offsets are immediates, every output is valid, loops fully unrolled: the inner loop
+// is 6 LDS.128 + 64 FMUL/FADD per chunk.
+// ---------------------------------------------------------------------------
+template <int D_H, int Z>
+struct FixedMlp {
+    static_assert(D_H % 16 == 0, "hoisting needs whole 16-element user blocks");
+    static constexpr int H = 64;
+    static constexpr int NCH0 = D_H / 4;     // item-half chunks of layer 0
+    static constexpr int NCHH = H / 4;       // hidden-layer input chunks
+    static constexpr int NCHZ = (Z + 3) / 4; // attention chunks
+    static constexpr int LDX0 = NCH0 | 1;
+    static constexpr int LDH = NCHH | 1;
+    // float4 offsets inside the fixed block
+    static constexpr int OFF_W0 = 0;
+    static constexpr int OFF_W1 = OFF_W0 + NCH0 * H;
+    static constexpr int OFF_W2 = OFF_W1 + NCHH * H;
+    static constexpr int OFF_A = OFF_W2 + NCHH * Z;
+    static constexpr int OFF_B0 = OFF_A + NCHZ;
+    static constexpr int OFF_B1 = OFF_B0 + H / 4;
+    static constexpr int OFF_B2 = OFF_B1 + H / 4;
+    static constexpr int OFF_ACC0 = OFF_B2 + NCHZ;
+    static constexpr int OFF_X0 = OFF_ACC0 + H;
+    static constexpr int OFF_H0 = OFF_X0 + GR_PT * LDX0;
+    static constexpr int OFF_H1 = OFF_H0 + GR_PT * LDH;
+    static constexpr int OFF_Z = OFF_H1 + GR_PT * LDH;
+    static constexpr int LDZ = NCHZ | 1;
+    static constexpr int OFF_SCORE = OFF_Z + GR_PT * LDZ;
+    static constexpr int TOTAL = OFF_SCORE + GR_PT / 4; // float4 units
+
+    // layer with O = 64 outputs: warp w -> pairs 4w..4w+3, lane -> outputs lane, lane+32
+    template <int NCH, int LDX, bool HAS_INIT>
+    static __device__ __forceinline__ void big(const float4 *__restrict__ X,
+                                               const float4 *__restrict__ W,
+                                               const float *__restrict__ bias,
+                                               const float4 *__restrict__ init,
+                                               float *__restrict__ Y) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        float4 a[4][2];
+        float4 i0 = make_float4(0.f, 0.f, 0.f, 0.f), i1 = i0;
+        if (HAS_INIT) { i0 = init[lane]; i1 = init[lane + 32]; }
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) { a[pp][0] = i0; a[pp][1] = i1; }
+        const float4 *xr = X + warp * 4 * LDX;
+        const float4 *wr = W + lane;
+#pragma unroll 8
+        for (int j = 0; j < NCH; ++j) {
+            const float4 w0 = wr[j * H], w1 = wr[j * H + 32];
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) {
+                const float4 x = xr[pp * LDX + j];
+                mac4(a[pp][0], x, w0);
+                mac4(a[pp][1], x, w1);
+            }
+        }
+        // epilogue: bias, ReLU, store in the next layer's processing order (K = 64)
+        const float b0 = bias[lane], b1 = bias[lane + 32];
+        const int j0 = chunk_perm(lane >> 2, H) * 4 + (lane & 3);
+        const int j1 = chunk_perm((lane + 32) >> 2, H) * 4 + (lane & 3);
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int p = warp * 4 + pp;
+            Y[p * LDH * 4 + j0] = relu_np(__fadd_rn(hsum4(a[pp][0]), b0));
+            Y[p * LDH * 4 + j1] = relu_np(__fadd_rn(hsum4(a[pp][1]), b1));
+        }
+    }
+
+    // run the tile: x0 holds item halves in processing order (user half hoisted into acc0)
+    static __device__ __forceinline__ void tile(float4 *base, int n_valid, int *nonfinite) {
+        float4 *x0 = base + OFF_X0, *h0 = base + OFF_H0, *h1 = base + OFF_H1;
+        big<NCH0, LDX0, true>(x0, base + OFF_W0, reinterpret_cast<const float *>(base + OFF_B0),
+                              base + OFF_ACC0, reinterpret_cast<float *>(h0));
+        __syncthreads();
+        big<NCHH, LDH, false>(h0, base + OFF_W1, reinterpret_cast<const float *>(base + OFF_B1),
+                              nullptr, reinterpret_cast<float *>(h1));
+        __syncthreads();
+        // final layer (Z heads, no ReLU): thread per (pair, head); W2 reads broadcast
+        if (threadIdx.x < GR_PT * Z) {
+            const int p = threadIdx.x % GR_PT, o = threadIdx.x / GR_PT;
+            const float4 *hr = h1 + p * LDH;
+            const float4 *W2 = base + OFF_W2;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < NCHH; ++j) mac4(acc, hr[j], W2[j * Z + o]);
+            const float z = __fadd_rn(hsum4(acc), reinterpret_cast<const float *>(base + OFF_B2)[o]);
+            reinterpret_cast<float *>(base + OFF_Z)[p * LDZ * 4 + o] = z;
+        }
+        __syncthreads();
+        // finiteness (metric.py:134-135) + attention (metric.py:150-154), thread per pair
+        if (threadIdx.x < GR_PT) {
+            const int p = threadIdx.x;
+            const float *z = reinterpret_cast<const float *>(base + OFF_Z) + p * LDZ * 4;
+            bool bad = false;
+#pragma unroll
+            for (int o = 0; o < Z; ++o) bad |= !isfinite(z[o]);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4 *A = base + OFF_A;
+#pragma unroll
+            for (int j = 0; j < NCHZ; ++j) {
+                const int c = chunk_perm(j, Z);
+                float e[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e[u] = (4 * c + u < Z) ? z[4 * c + u] : 0.f;
+                mac4(acc, make_float4(e[0], e[1], e[2], e[3]), A[j]);
+            }
+            reinterpret_cast<float *>(base + OFF_SCORE)[p] = hsum4(acc);
+            if (bad && p < n_valid) atomicOr(nonfinite, 1);
+        }
+    }
+};

@@ -91,7 +91,8 @@ __device__ __forceinline__ void warp_append2(bool ok, int32_t v, int32_t i, int 
     }
 }
 
-template <int MINB>
+// DH > 0 selects the compile-time-shaped scorer FixedMlp<DH, ZZ> (host lays out smem to match)
+template <int MINB, int DH, int ZZ>
 __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CtaState st;
@@ -229,7 +230,11 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     }
                 }
                 __syncthreads();
-                mlp_tile(M, S, sWm, sbm, sA, sW0, x0_nch, pre > 0 ? sAcc0 : nullptr, nv, a.nonfinite);
+                if constexpr (DH > 0)
+                    FixedMlp<DH, ZZ>::tile(reinterpret_cast<float4 *>(smem), nv, a.nonfinite);
+                else
+                    mlp_tile(M, S, sWm, sbm, sA, sW0, x0_nch, pre > 0 ? sAcc0 : nullptr, nv,
+                             a.nonfinite);
                 __syncthreads();
                 if (tid < nv) {
                     const int32_t s = fr_v[base + tid];

@@ -52,6 +52,9 @@ class GraphIndex:
         self._cnts = [np.empty(0, dtype=np.int32) for _ in range(max_layers)]
         self._slot_map = None
         self._dev = {}
+        # embedding row per slot; None = the item id (model_scorer convention, search.py:88).
+        # Catalog shards set it to the local row while ids stay global.
+        self.rows = None
 
     def _deg_cap(self, layer: int) -> int:
         return 2 * self.m if layer == 0 else self.m
@@ -288,6 +291,6 @@ class GraphIndex:
             if self._n == 0:
                 raise InvalidArgumentError("index is empty")
             ids, levels, layers, entry = self.graph_view()
-            h = _lib.DeviceGraph(layers, levels, entry, ids, device=device)
+            h = _lib.DeviceGraph(layers, levels, entry, ids, rows=self.rows, device=device)
             self._dev[device] = h
         return h
