@@ -116,6 +116,7 @@ def dist_setup(n_gpus):
         local = int(os.environ.get("LOCAL_RANK", str(rank)))
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return dist, rank, dist.get_world_size(), local
     torch.cuda.set_device(0)

@@ -129,6 +129,82 @@ def knn_ivf(x, K: int, seed: int = 0, probes: int = 3):
     return torch.gather(cand_i, 1, j), v
 
 
+def knn_backward_exact(x, K: int, block: int = 4096):
+    """K nearest among EARLIER members (j < i): the neighbours an HNSW insertion in slot
+    order would see (index.py:283-319 inserts in id order and links the new node to its
+    nearest already-inserted nodes, keep-M selection index.py:226-239)."""
+    torch = _torch()
+    M = x.shape[0]
+    nx = _sqnorm(x)
+    idx = torch.full((M, K), -1, dtype=torch.int64, device=x.device)
+    dd = torch.full((M, K), float("inf"), dtype=torch.float32, device=x.device)
+    for s in range(1, M, block):
+        e = min(M, s + block)
+        d2 = nx[s:e, None] + nx[None, :e] - 2.0 * (x[s:e] @ x[:e].T)
+        mask = torch.arange(e, device=x.device)[None, :] >= torch.arange(s, e, device=x.device)[:, None]
+        d2 = d2.masked_fill(mask, float("inf"))
+        kk = min(K, e)
+        v, i = torch.topk(d2, kk, dim=1, largest=False)
+        i = torch.where(torch.isfinite(v), i, torch.full_like(i, -1))
+        idx[s:e, :kk] = i
+        dd[s:e, :kk] = v
+    return idx, dd
+
+
+def knn_backward_ivf(x, K: int, seed: int = 0, probes: int = 4, exact_prefix: int = 131072):
+    """Backward K-NN at scale: exact for the first `exact_prefix` nodes, then geometric
+    stages [P, 2P) whose IVF index covers only the prefix [0, 2P) (so at least half of every
+    cell is eligible), masked to j < i."""
+    torch = _torch()
+    M, dev = x.shape[0], x.device
+    P0 = min(M, exact_prefix)
+    idx = torch.full((M, K), -1, dtype=torch.int64, device=dev)
+    dd = torch.full((M, K), float("inf"), dtype=torch.float32, device=dev)
+    i0, d0 = knn_backward_exact(x[:P0], K)
+    idx[:P0], dd[:P0] = i0, d0
+    lo = P0
+    nx = _sqnorm(x)
+    while lo < M:
+        hi = min(M, 2 * lo)
+        pre = x[:hi]
+        C = max(16, int(2 ** round(math.log2(max(16.0, math.sqrt(hi) * 1.3)))))
+        cent = _kmeans(pre, C, iters=5, seed=seed + lo)
+        prim = _assign(pre, cent, 1)[:, 0]
+        order = torch.argsort(prim)
+        counts = torch.bincount(prim, minlength=C)
+        starts = torch.cumsum(counts, 0) - counts
+        q = torch.arange(lo, hi, device=dev)
+        probe = _assign(x[lo:hi], cent, probes)  # [nq, P]
+        qcell = probe.reshape(-1)
+        qorder = torch.argsort(qcell)
+        qcounts = torch.bincount(qcell, minlength=C)
+        qstarts = torch.cumsum(qcounts, 0) - qcounts
+        nq = hi - lo
+        ci = torch.full((nq * probes, K), -1, dtype=torch.int64, device=dev)
+        cd = torch.full((nq * probes, K), float("inf"), dtype=torch.float32, device=dev)
+        ch, sh, qch, qsh = counts.tolist(), starts.tolist(), qcounts.tolist(), qstarts.tolist()
+        for c in range(C):
+            nm, nqc = ch[c], qch[c]
+            if nm == 0 or nqc == 0:
+                continue
+            mem = order[sh[c]:sh[c] + nm]
+            qp = qorder[qsh[c]:qsh[c] + nqc]
+            qpt = q[qp // probes]
+            for s in range(0, nqc, 8192):
+                qs = qpt[s:s + 8192]
+                d2 = nx[qs, None] + nx[None, mem] - 2.0 * (x[qs] @ x[mem].T)
+                d2 = d2.masked_fill(mem[None, :] >= qs[:, None], float("inf"))
+                kk = min(K, nm)
+                v, i = torch.topk(d2, kk, dim=1, largest=False)
+                ci[qp[s:s + 8192], :kk] = torch.where(torch.isfinite(v), mem[i], -1)
+                cd[qp[s:s + 8192], :kk] = v
+        v, j = torch.topk(cd.view(nq, probes * K), K, dim=1, largest=False)
+        idx[lo:hi] = torch.gather(ci.view(nq, probes * K), 1, j)
+        dd[lo:hi] = v
+        lo = hi
+    return idx, dd
+
+
 def symmetric_prune(idx, dd, cap: int):
     """Undirected union of k-NN edges, keep (u,v) iff it is within the `cap` nearest
     incident edges of both u and v -> symmetric rows with degree <= cap."""
@@ -179,31 +255,29 @@ def symmetric_prune(idx, dd, cap: int):
     return rows, deg.to(torch.int32)
 
 
-def long_links(x, n_links: int, seed: int, scales=(64, 1024)):
-    """Navigability links (the role HNSW's early insertions play): every node links to its
-    nearest members of sparse random samples of the layer (1/64, 1/1024 of it), so clusters
-    that a k-NN graph leaves disconnected get bridged at several length scales."""
+def long_links(x, n_links: int, seed: int, n_random: int = 256, block: int = 8192):
+    """Navigability links (the role HNSW's early insertions play): every node links to the
+    nearest members of its OWN random subset of the layer (n_random draws).  Nearest-of-a-
+    sparse-random-sample edges span the gaps a k-NN graph leaves between clusters, and since
+    every node draws a different subset no node becomes a hub that symmetric pruning would
+    strip."""
     torch = _torch()
     M, dev = x.shape[0], x.device
     g = torch.Generator(device=dev)
     g.manual_seed(seed + 7919)
-    per = max(1, n_links // len(scales))
-    idx_parts, d_parts = [], []
-    for sc in scales:
-        S = max(per + 1, M // sc)
-        if S >= M:
-            continue
-        samp = torch.randperm(M, generator=g, device=dev)[:S]
-        near = _assign(x, x[samp], per + 1)           # nearest sample points
-        cand = samp[near]                               # [M, per+1]
-        cand = torch.where(cand == torch.arange(M, device=dev)[:, None], -1, cand)
-        d2 = ((x[:, None, :] - x[cand.clamp_min(0)]) ** 2).sum(-1)
-        d2 = torch.where(cand < 0, float("inf"), d2)
-        idx_parts.append(cand)
-        d_parts.append(d2)
-    if not idx_parts:
-        return None
-    return torch.cat(idx_parts, 1), torch.cat(d_parts, 1)
+    S = min(n_random, M - 1)
+    K = min(n_links, S)
+    idx = torch.empty((M, K), dtype=torch.int64, device=dev)
+    dd = torch.empty((M, K), dtype=torch.float32, device=dev)
+    for s in range(0, M, block):
+        e = min(M, s + block)
+        cand = torch.randint(0, M, (e - s, S), generator=g, device=dev)
+        d2 = ((x[s:e, None, :] - x[cand]) ** 2).sum(-1)
+        d2 = torch.where(cand == torch.arange(s, e, device=dev)[:, None], float("inf"), d2)
+        v, i = torch.topk(d2, K, dim=1, largest=False)
+        idx[s:e] = torch.gather(cand, 1, i)
+        dd[s:e] = v
+    return idx, dd
 
 
 def merge_rows(r1, c1, r2, c2, cap: int):
@@ -225,7 +299,8 @@ def merge_rows(r1, c1, r2, c2, cap: int):
 
 
 def build_layers(vectors, m: int = 16, level_prob: float = 1.0 / 17.0, max_layers: int = 4,
-                 seed: int = 0, device=None, exact_limit: int = 200_000, long_frac: float = 0.0):
+                 seed: int = 0, device=None, exact_limit: int = 200_000, long_frac: float = 0.0,
+                 n_random: int = 256, mode: str = "hnsw"):
     """Return dict(levels, entry_slot, n_layers, nbrs=[(n, cap_l) int32], cnts=[(n,) int32])."""
     torch = _torch()
     dev = torch.device(device if device is not None else "cuda")
@@ -247,13 +322,17 @@ def build_layers(vectors, m: int = 16, level_prob: float = 1.0 / 17.0, max_layer
         if M >= 2:
             xm = x[mem]
             K = min(cap, M - 1)
-            if M <= exact_limit:
+            if mode == "hnsw":  # backward (insertion-order) k-NN, m per node like keep-M
+                Kb = min(m, M - 1)
+                idx, dd = (knn_backward_exact(xm, Kb) if M <= exact_limit
+                           else knn_backward_ivf(xm, Kb, seed=seed + l))
+            elif M <= exact_limit:
                 idx, dd = knn_exact(xm, K)
             else:
                 idx, dd = knn_ivf(xm, K, seed=seed + l)
             c_long = int(cap * long_frac) if M > 4 * cap else 0
             r, c = symmetric_prune(idx, dd, cap - c_long)
-            ll = long_links(xm, c_long, seed + 31 * l) if c_long else None
+            ll = long_links(xm, c_long, seed + 31 * l, n_random) if c_long else None
             if ll is not None:
                 rl, cl = symmetric_prune(ll[0], ll[1], c_long)
                 r, c = merge_rows(r, c, rl, cl, cap)
