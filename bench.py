@@ -194,7 +194,8 @@ def run_reference(args):
 
 def config_of(args, wl):
     N, d = wl.index._n, wl.model.d_h
-    return {"workload": f"{args.config}: {N} items, {d}-d, degree-{2 * wl.index.m} graph "
+    return {"mode": getattr(args, "mode", "exact"),
+            "workload": f"{args.config}: {N} items, {d}-d, degree-{2 * wl.index.m} graph "
                         f"(m={wl.index.m}), Z={wl.model.z_dim} MLP(64,64), top-100, "
                         f"{len(wl.users)} queries per GPU",
             "params": dict(PARAMS), "n_items": N, "d_h": d, "queries_per_gpu": len(wl.users),
@@ -227,7 +228,7 @@ def run_gmpgr(args):
     out_sc = torch.empty((Q, k), dtype=torch.float64, device=f"cuda:{dev}")
     out_cnt = torch.empty(Q, dtype=torch.int32, device=f"cuda:{dev}")
     out_st = torch.empty((Q, 5 + L), dtype=torch.int64, device=f"cuda:{dev}")
-    pc = SearchParams(**PARAMS)._c()
+    pc = SearchParams(**PARAMS, mode=args.mode)._c()
     stream = torch.cuda.current_stream(dev)
     sp = ctypes.c_void_p(stream.cuda_stream)
     lib = _lib.lib()
@@ -339,7 +340,11 @@ def run_gmpgr(args):
                 "d2h_bytes_per_step": d2h},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
+        "scoring_mode": args.mode,
     }
+    if args.mode == "tc":
+        c = searcher.counters()
+        line["tc_scoring"] = dict(c, exact_rescored_frac=c["exact_rescored"] / max(1, c["tensor_scored"]))
     if want_cpu and rank == 0:
         r, n, t, threads = cpu_baseline(wl, target_s=args.cpu_s)
         same = np.mean([np.array_equal(r["ids"][q], h_ids[q].numpy()) for q in range(n)])
@@ -368,6 +373,9 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="exact", choices=["exact", "tc"],
+                    help="exact: CUDA-core exact-fp32 scoring; tc: tcgen05 split-bf16 scoring "
+                         "with exact re-scoring of every near-threshold item")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -50,13 +50,22 @@ typedef struct gr_graph gr_graph;
 typedef struct gr_items gr_items;
 typedef struct gr_searcher gr_searcher;
 
-/* Search knobs = SearchParams (search.py:30-49); ef is frontier_width (ef or 2k). */
+/* Search knobs = SearchParams (search.py:30-49); ef is frontier_width (ef or 2k).
+ * mode: GR_MODE_EXACT (every claim scored by the exact-fp32 CUDA-core scorer) or
+ * GR_MODE_TC (tcgen05 split-bf16 scores; every item within band_rel*|T| + band_abs of a
+ * selection threshold T is re-scored exactly, so ids, order and returned scores are the
+ * exact ones whenever |approx - exact| < band/2).  band_* <= 0 selects the defaults. */
 typedef struct {
     int32_t k;
     int32_t k_parallel;
     int32_t hops;
     int32_t ef;
+    int32_t mode;
+    float band_rel;
+    float band_abs;
 } gr_search_params;
+
+enum { GR_MODE_EXACT = 0, GR_MODE_TC = 1 };
 
 const char *gr_last_error(void);
 int gr_abi_version(void);
@@ -121,6 +130,9 @@ int gr_search_async(gr_searcher *s, const gr_graph *g, const gr_model *m, const 
 int gr_searcher_status(gr_searcher *s, void *stream);
 /* kernel launches issued by this searcher so far (evidence counter for bench.py) */
 int64_t gr_searcher_launches(const gr_searcher *s);
+/* cumulative scoring counters of this searcher: out[0] = exact re-scores (tensor-core
+ * mode), out[1] = tensor-core scores.  Synchronises the device. */
+int gr_searcher_counters(gr_searcher *s, int64_t *out);
 
 /* Exact top-k over ALL items of the handle for Q users (ground truth, search.py:93-108):
  * ids int64 [Q, k] (= item rows), scores fp64 [Q, k].  host-or-device pointers. */

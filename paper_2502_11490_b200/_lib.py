@@ -28,13 +28,18 @@ EXPORTS = (
     "gr_score_pairs",
     "gr_searcher_create", "gr_searcher_destroy",
     "gr_search", "gr_search_async", "gr_searcher_status", "gr_searcher_launches",
+    "gr_searcher_counters",
     "gr_brute_force", "gr_merge_topk",
 )
 
 
+GR_MODE_EXACT, GR_MODE_TC = 0, 1
+
+
 class SearchParamsC(C.Structure):
     _fields_ = [("k", C.c_int32), ("k_parallel", C.c_int32), ("hops", C.c_int32),
-                ("ef", C.c_int32)]
+                ("ef", C.c_int32), ("mode", C.c_int32), ("band_rel", C.c_float),
+                ("band_abs", C.c_float)]
 
 
 _lib = None
@@ -61,6 +66,7 @@ def _declare(lib):
         "gr_search_async": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, vp]),
         "gr_searcher_status": (C.c_int, [vp, vp]),
         "gr_searcher_launches": (i64, [vp]),
+        "gr_searcher_counters": (C.c_int, [vp, vp]),
         "gr_brute_force": (C.c_int, [vp, vp, vp, i64, i32, vp, vp, C.c_int, vp]),
         "gr_merge_topk": (C.c_int, [C.c_int, vp, vp, i32, i64, i32, i32, vp, vp, vp, vp]),
     }
@@ -224,3 +230,8 @@ class DeviceSearcher(_Handle):
     @property
     def launches(self) -> int:
         return int(lib().gr_searcher_launches(self.h))
+
+    def counters(self) -> dict:
+        out = np.zeros(2, dtype=np.int64)
+        check(lib().gr_searcher_counters(self.h, ptr(out)))
+        return {"exact_rescored": int(out[0]), "tensor_scored": int(out[1])}

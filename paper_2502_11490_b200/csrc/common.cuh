@@ -76,6 +76,10 @@ struct DevModel {
     const float *b[GR_MAX_MLP];  // [dims[m+1]]
     const float4 *A;             // [nch[n_mlp]] attention in processing order
     int pre_ch;                  // layer-0 chunks that see only h_u (4 * floor(d_h/16))
+    // tensor-core operands (tc_scorer.cuh), present when the model has the TcMlp shape
+    const void *tcB;             // bf16 hi/lo core-matrix images: W0 item half, W1
+    const float *tcMisc;         // b1[64] | W2[Z][64] | b2[4] | attention[4]
+    int tc_ok;
 };
 
 // Device graph: layer 0 as fixed-width rows padded with -1 (no count reads);

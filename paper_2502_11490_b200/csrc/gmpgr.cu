@@ -35,6 +35,31 @@ int fail(int code, const std::string &msg) {
     } while (0)
 
 int round4(int x) { return (x + 3) & ~3; }
+
+uint16_t bf16_rne(float x) {
+    uint32_t u;
+    std::memcpy(&u, &x, 4);
+    u += 0x7FFFu + ((u >> 16) & 1u);
+    return (uint16_t)(u >> 16);
+}
+float bf16_to_f(uint16_t h) {
+    uint32_t u = (uint32_t)h << 16;
+    float f;
+    std::memcpy(&f, &u, 4);
+    return f;
+}
+// hi/lo bf16 images of a [rows x K] fp32 operand in the UMMA K-major core-matrix layout
+void pack_kmajor(const float *src, int rows, int K, int ld, int col0, uint8_t *hi, uint8_t *lo) {
+    for (int r = 0; r < rows; ++r)
+        for (int k = 0; k < K; ++k) {
+            const float x = src[(size_t)r * ld + col0 + k];
+            const uint16_t h = bf16_rne(x);
+            const uint16_t l = bf16_rne(x - bf16_to_f(h));
+            const uint32_t off = tc::kmaj_off(r, k, K);
+            std::memcpy(hi + off, &h, 2);
+            std::memcpy(lo + off, &l, 2);
+        }
+}
 int odd(int x) { return x | 1; }
 int pow2ceil(int x) {
     int p = 32;
@@ -75,6 +100,7 @@ struct gr_model {
     int device;
     DevModel dm;
     void *dbuf;
+    void *tcbuf[2] = {nullptr, nullptr};
     std::vector<int> dims;
 };
 
@@ -99,6 +125,8 @@ struct gr_searcher {
     int32_t *f_slot = nullptr, *f_srch = nullptr, *surv_v = nullptr, *surv_i = nullptr,
             *fr_v = nullptr, *fr_i = nullptr, *seg_v = nullptr, *pool_slot = nullptr;
     uint64_t *fr_key = nullptr, *seg_key = nullptr, *pool_key = nullptr;
+    int32_t *pool_meta = nullptr;
+    unsigned long long *counters = nullptr;
     int *flags = nullptr; // [0] queue, [1] nonfinite, [2] bad index
     int64_t launches = 0;
     // staging for host-pointer calls
@@ -106,12 +134,13 @@ struct gr_searcher {
     size_t st_users_n = 0, st_out_n = 0, st_stats_n = 0;
     void free_scratch() {
         void *ps[] = {tags, epochs, f_slot, f_srch, surv_v, surv_i, fr_v, fr_i, seg_v, pool_slot,
-                      fr_key, seg_key, pool_key};
+                      fr_key, seg_key, pool_key, pool_meta};
         for (void *p : ps)
             if (p) cudaFree(p);
         tags = nullptr; epochs = nullptr; f_slot = f_srch = surv_v = surv_i = fr_v = fr_i = seg_v =
             pool_slot = nullptr;
         fr_key = seg_key = pool_key = nullptr;
+        pool_meta = nullptr;
         slots = n = capF = capS = capP = 0;
     }
 };
@@ -179,6 +208,32 @@ int gr_model_create(int device, int n_mlp, const int32_t *dims, const float *con
     M->dbuf = d;
     DevModel &dm = M->dm;
     std::memset(&dm, 0, sizeof(dm));
+    // tensor-core operand images (TcMlp shape: 3 layers, hidden 64/64, d_h in {64,128}, Z 2..3)
+    const int dh = dims[0] / 2;
+    if (n_mlp == 3 && relu && dims[1] == 64 && dims[2] == 64 && (dh == 64 || dh == 128) &&
+        (Z == 2 || Z == 3)) {
+        const size_t b0 = (size_t)64 * dh * 2, b1 = (size_t)64 * 64 * 2;
+        std::vector<uint8_t> img(2 * b0 + 2 * b1, 0);
+        pack_kmajor(W[0], 64, dh, 2 * dh, dh, img.data(), img.data() + b0);
+        pack_kmajor(W[1], 64, 64, 64, 0, img.data() + 2 * b0, img.data() + 2 * b0 + b1);
+        std::vector<float> misc(64 + 64 * Z + 8, 0.f);
+        std::memcpy(misc.data(), b[1], 64 * 4);
+        std::memcpy(misc.data() + 64, W[2], (size_t)64 * Z * 4);
+        std::memcpy(misc.data() + 64 + 64 * Z, b[2], (size_t)Z * 4);
+        std::memcpy(misc.data() + 68 + 64 * Z, attention, (size_t)Z * 4);
+        uint8_t *dimg = nullptr;
+        float *dmisc = nullptr;
+        if (dmalloc(&dimg, img.size()) || dmalloc(&dmisc, misc.size())) {
+            cudaFree(d); delete M; return GR_ENOMEM;
+        }
+        cudaMemcpy(dimg, img.data(), img.size(), cudaMemcpyHostToDevice);
+        cudaMemcpy(dmisc, misc.data(), misc.size() * 4, cudaMemcpyHostToDevice);
+        M->tcbuf[0] = dimg;
+        M->tcbuf[1] = dmisc;
+        dm.tcB = dimg;
+        dm.tcMisc = dmisc;
+        dm.tc_ok = 1;
+    }
     dm.n_mlp = n_mlp;
     dm.relu = relu ? 1 : 0;
     dm.d_h = dims[0] / 2;
@@ -198,6 +253,8 @@ int gr_model_destroy(gr_model *m) {
     if (!m) return GR_OK;
     cudaSetDevice(m->device);
     cudaFree(m->dbuf);
+    if (m->tcbuf[0]) cudaFree(m->tcbuf[0]);
+    if (m->tcbuf[1]) cudaFree(m->tcbuf[1]);
     delete m;
     return GR_OK;
 }
@@ -421,9 +478,23 @@ void plan_fixed(SearchArgs &a) {
     a.off_score = F::OFF_SCORE * 16;
 }
 
-int plan_search(const DevModel &M, int k, int kp, SearchArgs &a, int shape) {
+template <int DH, int ZZ>
+void plan_tc(SearchArgs &a, SmemPlan &P) {
+    using T = TcMlp<DH, ZZ>;
+    a.off_acc0 = T::OFF_ACC0;
+    P.bytes = T::BYTES;
+}
+
+int plan_search(const DevModel &M, int k, int kp, SearchArgs &a, int shape, int mode) {
     SmemPlan P;
-    if (shape) {
+    if (mode == GR_MODE_TC) {
+        switch (shape) {
+        case 1283: plan_tc<128, 3>(a, P); break;
+        case 1282: plan_tc<128, 2>(a, P); break;
+        case 643: plan_tc<64, 3>(a, P); break;
+        default: plan_tc<64, 2>(a, P); break;
+        }
+    } else if (shape) {
         switch (shape) {
         case 1283: plan_fixed<128, 3>(a); P.bytes = FixedMlp<128, 3>::TOTAL * 16; break;
         case 1282: plan_fixed<128, 2>(a); P.bytes = FixedMlp<128, 2>::TOTAL * 16; break;
@@ -527,6 +598,7 @@ int ensure_search_scratch(gr_searcher *S, const gr_graph *G, int64_t slots, int6
     if ((rc = dmalloc(&S->seg_key, (size_t)slots * capS))) return rc;
     if ((rc = dmalloc(&S->pool_key, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&S->pool_slot, (size_t)slots * 2 * capP))) return rc;
+    if ((rc = dmalloc(&S->pool_meta, (size_t)slots * 2 * capP))) return rc;
     GR_CUDA(cudaMemset(S->tags, 0, (size_t)slots * n * 8));
     GR_CUDA(cudaMemset(S->epochs, 0, (size_t)slots * 4));
     S->slots = slots;
@@ -544,6 +616,7 @@ int check_params(const gr_search_params *p) {
     if (p->k_parallel > p->k) return fail(GR_EINVAL, "k_parallel must not exceed k");
     if (p->ef < 1) return fail(GR_EINVAL, "ef must be >= 1");
     if (p->k > 8192) return fail(GR_EINVAL, "k > 8192 not supported on the device path");
+    if (p->mode != GR_MODE_EXACT && p->mode != GR_MODE_TC) return fail(GR_EINVAL, "unknown mode");
     return GR_OK;
 }
 
@@ -554,15 +627,28 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
     const int shape = fixed_shape(M->dm);
-    const int smem = plan_search(M->dm, p->k, p->k_parallel, a, shape);
+    const int mode = p->mode;
+    if (mode == GR_MODE_TC && (!shape || !M->dm.tc_ok))
+        return fail(GR_EINVAL, "tensor-core mode needs the (d_h in {64,128}, hidden (64,64), Z in {2,3}) model shape");
+    const int smem = plan_search(M->dm, p->k, p->k_parallel, a, shape, mode);
     void (*kern)(const SearchArgs) = nullptr;
-    switch (shape) {
-    case 1283: kern = hipanns_search_kernel<2, 128, 3>; break;
-    case 1282: kern = hipanns_search_kernel<2, 128, 2>; break;
-    case 643: kern = hipanns_search_kernel<2, 64, 3>; break;
-    case 642: kern = hipanns_search_kernel<2, 64, 2>; break;
-    default:
-        kern = smem <= 110 * 1024 ? hipanns_search_kernel<2, 0, 0> : hipanns_search_kernel<1, 0, 0>;
+    if (mode == GR_MODE_TC) {
+        switch (shape) {
+        case 1283: kern = hipanns_search_kernel<2, 128, 3, 1>; break;
+        case 1282: kern = hipanns_search_kernel<2, 128, 2, 1>; break;
+        case 643: kern = hipanns_search_kernel<2, 64, 3, 1>; break;
+        default: kern = hipanns_search_kernel<2, 64, 2, 1>; break;
+        }
+    } else {
+        switch (shape) {
+        case 1283: kern = hipanns_search_kernel<2, 128, 3, 0>; break;
+        case 1282: kern = hipanns_search_kernel<2, 128, 2, 0>; break;
+        case 643: kern = hipanns_search_kernel<2, 64, 3, 0>; break;
+        case 642: kern = hipanns_search_kernel<2, 64, 2, 0>; break;
+        default:
+            kern = smem <= 110 * 1024 ? hipanns_search_kernel<2, 0, 0, 0>
+                                      : hipanns_search_kernel<1, 0, 0, 0>;
+        }
     }
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 0;
@@ -600,6 +686,10 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     a.seg_key = S->seg_key;
     a.pool_key = S->pool_key;
     a.pool_slot = S->pool_slot;
+    a.pool_meta = S->pool_meta;
+    a.counters = S->counters;
+    a.band_rel = p->band_rel > 0.f ? p->band_rel : 1e-3f;
+    a.band_abs = p->band_abs > 0.f ? p->band_abs : 1e-3f;
     a.capF = S->capF;
     a.capS = S->capS;
     a.capP = S->capP;
@@ -623,6 +713,8 @@ int gr_searcher_create(int device, gr_searcher **out) {
     S->device = device;
     if (int rc = dmalloc(&S->flags, 4)) { delete S; return rc; }
     cudaMemset(S->flags, 0, 16);
+    if (int rc = dmalloc(&S->counters, 2)) { cudaFree(S->flags); delete S; return rc; }
+    cudaMemset(S->counters, 0, 16);
     *out = S;
     return GR_OK;
 }
@@ -632,6 +724,7 @@ int gr_searcher_destroy(gr_searcher *s) {
     cudaSetDevice(s->device);
     s->free_scratch();
     cudaFree(s->flags);
+    cudaFree(s->counters);
     s->st_users.release();
     s->st_ids.release();
     s->st_scores.release();
@@ -642,6 +735,14 @@ int gr_searcher_destroy(gr_searcher *s) {
 }
 
 int64_t gr_searcher_launches(const gr_searcher *s) { return s ? s->launches : 0; }
+
+int gr_searcher_counters(gr_searcher *s, int64_t *out) {
+    if (!s || !out) return fail(GR_EINVAL, "null argument");
+    GR_CUDA(cudaSetDevice(s->device));
+    GR_CUDA(cudaDeviceSynchronize());
+    GR_CUDA(cudaMemcpy(out, s->counters, 16, cudaMemcpyDeviceToHost));
+    return GR_OK;
+}
 
 int gr_search_async(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_items *it,
                     const float *users, int64_t Q, const gr_search_params *p, int64_t *out_ids,

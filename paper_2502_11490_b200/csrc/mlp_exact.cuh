@@ -205,36 +205,33 @@ struct FixedMlp {
         }
     }
 
-    // run the tile: x0 holds item halves in processing order (user half hoisted into acc0)
-    static __device__ __forceinline__ void tile(float4 *base, int n_valid, int *nonfinite) {
-        float4 *x0 = base + OFF_X0, *h0 = base + OFF_H0, *h1 = base + OFF_H1;
-        big<NCH0, LDX0, true>(x0, base + OFF_W0, reinterpret_cast<const float *>(base + OFF_B0),
-                              base + OFF_ACC0, reinterpret_cast<float *>(h0));
+    // run the tile with weights/buffers at explicit addresses (smem or global weights)
+    static __device__ __forceinline__ void tile_p(const float4 *W0, const float4 *W1,
+                                                  const float4 *W2, const float4 *A,
+                                                  const float *b0, const float *b1,
+                                                  const float *b2, const float4 *acc0,
+                                                  float4 *x0, float4 *h0, float4 *h1, float *zb,
+                                                  float *score, int n_valid, int *nonfinite) {
+        big<NCH0, LDX0, true>(x0, W0, b0, acc0, reinterpret_cast<float *>(h0));
         __syncthreads();
-        big<NCHH, LDH, false>(h0, base + OFF_W1, reinterpret_cast<const float *>(base + OFF_B1),
-                              nullptr, reinterpret_cast<float *>(h1));
+        big<NCHH, LDH, false>(h0, W1, b1, nullptr, reinterpret_cast<float *>(h1));
         __syncthreads();
-        // final layer (Z heads, no ReLU): thread per (pair, head); W2 reads broadcast
         if (threadIdx.x < GR_PT * Z) {
             const int p = threadIdx.x % GR_PT, o = threadIdx.x / GR_PT;
             const float4 *hr = h1 + p * LDH;
-            const float4 *W2 = base + OFF_W2;
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
             for (int j = 0; j < NCHH; ++j) mac4(acc, hr[j], W2[j * Z + o]);
-            const float z = __fadd_rn(hsum4(acc), reinterpret_cast<const float *>(base + OFF_B2)[o]);
-            reinterpret_cast<float *>(base + OFF_Z)[p * LDZ * 4 + o] = z;
+            zb[p * LDZ * 4 + o] = __fadd_rn(hsum4(acc), b2[o]);
         }
         __syncthreads();
-        // finiteness (metric.py:134-135) + attention (metric.py:150-154), thread per pair
         if (threadIdx.x < GR_PT) {
             const int p = threadIdx.x;
-            const float *z = reinterpret_cast<const float *>(base + OFF_Z) + p * LDZ * 4;
+            const float *z = zb + p * LDZ * 4;
             bool bad = false;
 #pragma unroll
             for (int o = 0; o < Z; ++o) bad |= !isfinite(z[o]);
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-            const float4 *A = base + OFF_A;
 #pragma unroll
             for (int j = 0; j < NCHZ; ++j) {
                 const int c = chunk_perm(j, Z);
@@ -243,8 +240,18 @@ struct FixedMlp {
                 for (int u = 0; u < 4; ++u) e[u] = (4 * c + u < Z) ? z[4 * c + u] : 0.f;
                 mac4(acc, make_float4(e[0], e[1], e[2], e[3]), A[j]);
             }
-            reinterpret_cast<float *>(base + OFF_SCORE)[p] = hsum4(acc);
+            score[p] = hsum4(acc);
             if (bad && p < n_valid) atomicOr(nonfinite, 1);
         }
+    }
+
+    // run the tile: x0 holds item halves in processing order (user half hoisted into acc0)
+    static __device__ __forceinline__ void tile(float4 *base, int n_valid, int *nonfinite) {
+        tile_p(base + OFF_W0, base + OFF_W1, base + OFF_W2, base + OFF_A,
+               reinterpret_cast<const float *>(base + OFF_B0),
+               reinterpret_cast<const float *>(base + OFF_B1),
+               reinterpret_cast<const float *>(base + OFF_B2), base + OFF_ACC0, base + OFF_X0,
+               base + OFF_H0, base + OFF_H1, reinterpret_cast<float *>(base + OFF_Z),
+               reinterpret_cast<float *>(base + OFF_SCORE), n_valid, nonfinite);
     }
 };

@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "mlp_exact.cuh"
 #include "select.cuh"
+#include "tc_scorer.cuh"
 
 struct SearchArgs {
     DevGraph g;
@@ -47,6 +48,9 @@ struct SearchArgs {
     uint64_t *seg_key; // [slots][capS]
     uint64_t *pool_key; // [slots][2][capP]
     int32_t *pool_slot; // [slots][2][capP]
+    int32_t *pool_meta; // [slots][2][capP]: eval hop << 1 | exact (tensor-core mode)
+    unsigned long long *counters; // [0] exact re-scores, [1] tensor-core scores
+    float band_rel, band_abs;     // refinement band: |s - T| <= band_rel*|T| + band_abs
     int64_t capF, capS, capP;
     int *queue;
     int *nonfinite;
@@ -92,7 +96,11 @@ __device__ __forceinline__ void warp_append2(bool ok, int32_t v, int32_t i, int 
 }
 
 // DH > 0 selects the compile-time-shaped scorer FixedMlp<DH, ZZ> (host lays out smem to match)
-template <int MINB, int DH, int ZZ>
+// MODE 0: exact-fp32 scoring of every claim.  MODE 1 (DH > 0): tcgen05 split-bf16 scores,
+// then exact re-scoring of every item inside the band around each selection threshold
+// (frontier top-ef, pool top-k, seeds top-kp, final top-k), so all decisions and all
+// returned scores are the exact ones provided |approx - exact| < band / 2.
+template <int MINB, int DH, int ZZ, int MODE>
 __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CtaState st;
@@ -105,7 +113,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
     const float4 *sWm[GR_MAX_MLP];
     const float *sbm[GR_MAX_MLP];
     const int O0 = M.dims[1], K0 = M.dims[0], nch0 = M.nch[0], pre = M.pre_ch;
-    {
+    if constexpr (MODE == 0) {
         const int n0 = (nch0 - pre) * O0;
         for (int t = tid; t < n0; t += GR_NT) sW0[t] = M.W[0][pre * O0 + t];
         for (int m = 0; m < M.n_mlp; ++m) {
@@ -140,11 +148,41 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
     int32_t *seg_off = seg_cnt + a.kp;
     int32_t *fn_off = seg_off + a.kp;
     const int x0_nch = nch0 - pre;
-    // zero activation buffers once (padding lanes stay zero)
-    for (int t = tid; t < GR_PT * a.ldx0; t += GR_NT) S.x0[t] = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int t = tid; t < GR_PT * a.ldh; t += GR_NT) {
-        S.h[0][t] = make_float4(0.f, 0.f, 0.f, 0.f);
-        S.h[1][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+    if constexpr (MODE == 0) {
+        // zero activation buffers once (padding lanes stay zero)
+        for (int t = tid; t < GR_PT * a.ldx0; t += GR_NT) S.x0[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int t = tid; t < GR_PT * a.ldh; t += GR_NT) {
+            S.h[0][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+            S.h[1][t] = make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+    }
+    // ---- tensor-core mode: operands, TMEM, mbarrier
+    uint32_t tmem = 0, phase = 0;
+    using TC = TcMlp<(DH > 0 ? DH : 64), (ZZ > 0 ? ZZ : 2)>;
+    using FX = FixedMlp<(DH > 0 ? DH : 64), (ZZ > 0 ? ZZ : 2)>;
+    if constexpr (MODE == 1) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(M.tcB);
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + TC::OFF_B0H);
+        for (int t = tid; t < (TC::OFF_AH - TC::OFF_B0H) / 16; t += GR_NT) dst[t] = src[t];
+        float *b1 = reinterpret_cast<float *>(smem + TC::OFF_B1);
+        for (int t = tid; t < 64; t += GR_NT) b1[t] = M.tcMisc[t];
+        float *w2 = reinterpret_cast<float *>(smem + TC::OFF_W2);
+        for (int t = tid; t < 64 * ZZ; t += GR_NT) w2[t] = M.tcMisc[64 + t];
+        if (tid < 4) {
+            reinterpret_cast<float *>(smem + TC::OFF_B2)[tid] = M.tcMisc[64 + 64 * ZZ + tid];
+            reinterpret_cast<float *>(smem + TC::OFF_ATT)[tid] = M.tcMisc[68 + 64 * ZZ + tid];
+        }
+        uint32_t *tptr = reinterpret_cast<uint32_t *>(smem + TC::OFF_TMEM);
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             tc::smem_u32(tptr)), "r"(128));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        if (tid == 0) tc::mbar_init(reinterpret_cast<uint64_t *>(smem + TC::OFF_BAR), 1);
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        tmem = *tptr;
     }
 
     // ---- per-slot scratch
@@ -159,6 +197,14 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
     uint64_t *seg_key = a.seg_key + slot * a.capS;
     uint64_t *pkey[2] = {a.pool_key + slot * 2 * a.capP, a.pool_key + slot * 2 * a.capP + a.capP};
     int32_t *pslot[2] = {a.pool_slot + slot * 2 * a.capP, a.pool_slot + slot * 2 * a.capP + a.capP};
+    int32_t *pmeta[2] = {nullptr, nullptr};
+    if constexpr (MODE == 1) {
+        pmeta[0] = a.pool_meta + slot * 2 * a.capP;
+        pmeta[1] = pmeta[0] + a.capP;
+    }
+    int32_t *rq = surv_v;           // re-score request list (survivor buffer is free then)
+    int32_t *seg_ex = fr_i;         // exact flags of seg entries (fr_i is dead after the scatter)
+    auto band_of = [&](float T) { return a.band_rel * fabsf(T) + a.band_abs; };
     const int d_h = M.d_h;
     const bool fast_fill = (d_h % 16) == 0;
     const int top = g.n_layers - 1;
@@ -193,12 +239,41 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 mac4(acc, x, M.W[0][j * O0 + o]);
             }
             sAcc0[o] = acc;
+            if constexpr (MODE == 1)
+                reinterpret_cast<float *>(smem + TC::OFF_U)[o] =
+                    __fadd_rn(hsum4(acc), M.b[0][o]);
         }
 
         // ---- score fr_v[0..nFresh) (hop h, layer L): keys, pool append, hop max
-        auto score_fresh = [&](int nFresh) {
+        auto score_fresh = [&](int nFresh, int hop) {
             const int pc = st.pool_cur;
             const uint64_t poolT = st.poolT;
+            if constexpr (MODE == 1) {
+                // approximate scores on the tensor cores, 128 pairs per tile
+                const float Ts = orderable_f32((uint32_t)(poolT >> 32));
+                const float lo_cut = poolT ? Ts - band_of(Ts) : -INFINITY;
+                const float *sc = reinterpret_cast<const float *>(smem + TC::OFF_SC);
+                for (int base = 0; base < nFresh; base += TC::TM) {
+                    const int nv = min(TC::TM, nFresh - base);
+                    TC::tile(smem, tmem, phase, a.it, g, fr_v + base, nv);
+                    if (tid < nv) {
+                        const int32_t s = fr_v[base + tid];
+                        const float v = sc[tid];
+                        if (!isfinite(v)) atomicOr(a.nonfinite, 1);
+                        const uint64_t key = make_key(v, slot_rank(g, s));
+                        fr_key[base + tid] = key;
+                        if (v >= lo_cut) { // relaxed pool filter: the exact score may be above poolT
+                            const int idx = atomicAdd(&st.nPool, 1);
+                            pkey[pc][idx] = key;
+                            pslot[pc][idx] = s;
+                            pmeta[pc][idx] = hop << 1;
+                        }
+                    }
+                }
+                if (tid == 0) atomicAdd(a.counters + 1, (unsigned long long)nFresh);
+                __syncthreads();
+                return;
+            }
             for (int base = 0; base < nFresh; base += GR_PT) {
                 const int nv = min(GR_PT, nFresh - base);
                 // gather item rows into x0 (processing order)
@@ -251,6 +326,65 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
             __syncthreads();
         };
 
+        // ---- exact re-scoring of rq[0..nrq) (indices into the pool (target 0) or seg arrays)
+        auto rescore = [&](int nrq, int target) {
+            if constexpr (MODE == 1) {
+                const int pc = st.pool_cur;
+                float4 *x0 = reinterpret_cast<float4 *>(smem + TC::OFF_EX_X0);
+                const float *esc = reinterpret_cast<const float *>(smem + TC::OFF_EX_SC);
+                for (int base = 0; base < nrq; base += GR_PT) {
+                    const int nv = min(GR_PT, nrq - base);
+                    for (int pp = 0; pp < 4; ++pp) {
+                        const int p = warp * 4 + pp;
+                        float4 *xr = x0 + p * FX::LDX0;
+                        if (p < nv) {
+                            const int idx = rq[base + p];
+                            const int32_t s = target == 0 ? pslot[pc][idx] : seg_v[idx];
+                            const float4 *hv = reinterpret_cast<const float4 *>(a.it.emb + slot_row(g, s) * a.it.ld);
+                            for (int cc = lane; cc < DH / 4; cc += 32)
+                                xr[chunk_perm(DH / 4 + cc, 2 * DH) - DH / 4] = __ldg(hv + cc);
+                        } else {
+                            for (int cc = lane; cc < DH / 4; cc += 32) xr[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                    }
+                    __syncthreads();
+                    FX::tile_p(M.W[0] + (DH / 4) * 64, M.W[1], M.W[2], M.A, M.b[0], M.b[1], M.b[2],
+                               sAcc0, x0, reinterpret_cast<float4 *>(smem + TC::OFF_EX_H0),
+                               reinterpret_cast<float4 *>(smem + TC::OFF_EX_H1),
+                               reinterpret_cast<float *>(smem + TC::OFF_EX_Z),
+                               reinterpret_cast<float *>(smem + TC::OFF_EX_SC), nv, a.nonfinite);
+                    __syncthreads();
+                    if (tid < nv) {
+                        const int idx = rq[base + tid];
+                        if (target == 0) {
+                            pkey[pc][idx] = make_key(esc[tid], slot_rank(g, pslot[pc][idx]));
+                            pmeta[pc][idx] |= 1;
+                        } else {
+                            seg_key[idx] = make_key(esc[tid], slot_rank(g, seg_v[idx]));
+                            seg_ex[idx] = 1;
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0 && nrq) atomicAdd(a.counters, (unsigned long long)nrq);
+            }
+        };
+        // collect pool entries that are not exact and satisfy pred(score) into rq
+        auto collect_pool = [&](auto pred) {
+            const int pc = st.pool_cur, np = st.nPool;
+            if (tid == 0) st.nS = 0;
+            __syncthreads();
+            for (int i0 = 0; i0 < np; i0 += GR_NT) {
+                const int i = i0 + tid;
+                bool ok = false;
+                if (i < np && !(pmeta[pc][i] & 1))
+                    ok = pred(orderable_f32((uint32_t)(pkey[pc][i] >> 32)));
+                warp_append2(ok, i, 0, &st.nS, rq, surv_i);
+            }
+            __syncthreads();
+            return st.nS;
+        };
+
         // ---- after scoring: best tracking, per-layer count, pool compaction to top-k
         auto after_score = [&](int layer, int h, int nFresh) {
             if (tid == 0) {
@@ -261,6 +395,12 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
             __syncthreads();
             if (st.nPool > a.k) {
                 const int pc = st.pool_cur;
+                if constexpr (MODE == 1) {
+                    const uint64_t Ta = cta_select_threshold(pkey[pc], st.nPool, a.k, hist, st.bcast);
+                    const float Ts = orderable_f32((uint32_t)(Ta >> 32)), bd = band_of(Ts);
+                    const int nrq = collect_pool([&](float v) { return fabsf(v - Ts) <= bd; });
+                    rescore(nrq, 0);
+                }
                 const uint64_t T = cta_select_threshold(pkey[pc], st.nPool, a.k, hist, st.bcast);
                 if (tid == 0) st.nPool2 = 0;
                 __syncthreads();
@@ -271,6 +411,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                         const int idx = atomicAdd(&st.nPool2, 1);
                         pkey[pc ^ 1][idx] = key;
                         pslot[pc ^ 1][idx] = pslot[pc][i];
+                        if constexpr (MODE == 1) pmeta[pc ^ 1][idx] = pmeta[pc][i];
                     }
                 }
                 __syncthreads();
@@ -336,7 +477,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         resolve(st.nS, 1);
         {
             const int nFresh = st.nFresh;
-            score_fresh(nFresh);
+            score_fresh(nFresh, 0);
             after_score(top, 0, nFresh);
         }
 
@@ -344,6 +485,19 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         for (int layer = top; layer >= 0; --layer) {
             // ---- seeds: sorted pool, first min(kp, |pool|)
             {
+                if constexpr (MODE == 1) {
+                    // seeds (and their order) must be exact: re-score the top-kp region + band
+                    const int np0 = st.nPool, pc0 = st.pool_cur;
+                    int nrq;
+                    if (np0 > a.kp) {
+                        const uint64_t Ta = cta_select_threshold(pkey[pc0], np0, a.kp, hist, st.bcast);
+                        const float Ts = orderable_f32((uint32_t)(Ta >> 32)), bd = band_of(Ts);
+                        nrq = collect_pool([&](float v) { return v >= Ts - bd; });
+                    } else {
+                        nrq = collect_pool([&](float) { return true; });
+                    }
+                    rescore(nrq, 0);
+                }
                 const int np = st.nPool, pc = st.pool_cur;
                 for (int i = tid; i < np; i += GR_NT) { sortk[i] = pkey[pc][i]; sortv[i] = pslot[pc][i]; }
                 __syncthreads();
@@ -401,7 +555,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 __syncthreads();
                 resolve(st.nS, 0);
                 const int nFresh = st.nFresh;
-                score_fresh(nFresh);
+                score_fresh(nFresh, h);
                 after_score(layer, h, nFresh);
                 if (t == a.hops - 1) break; // frontier after a layer's last hop is unused
                 // ---- per-searcher top-ef of fresh claims -> next frontier
@@ -429,6 +583,26 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     seg_key[pos] = fr_key[t2];
                 }
                 __syncthreads();
+                if constexpr (MODE == 1) {
+                    // exact re-score of the band around each searcher's ef-th approximate key
+                    for (int t2 = tid; t2 < nFresh; t2 += GR_NT) seg_ex[t2] = 0;
+                    if (tid == 0) st.nS = 0;
+                    __syncthreads();
+                    for (int i = warp; i < nsr; i += GR_NW) {
+                        const int ni = seg_cnt[i], off = seg_off[i];
+                        if (ni <= a.ef) continue;
+                        const uint64_t Ta = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
+                        const float Ts = orderable_f32((uint32_t)(Ta >> 32)), bd = band_of(Ts);
+                        for (int j0 = 0; j0 < ni; j0 += 32) {
+                            const int j = j0 + lane;
+                            const bool in = j < ni &&
+                                fabsf(orderable_f32((uint32_t)(seg_key[off + j] >> 32)) - Ts) <= bd;
+                            warp_append2(in, off + j, 0, &st.nS, rq, surv_i);
+                        }
+                    }
+                    __syncthreads();
+                    rescore(st.nS, 1);
+                }
                 const int fn = fc ^ 1;
                 for (int i = warp; i < nsr; i += GR_NW) {
                     const int ni = seg_cnt[i], off = seg_off[i], fo = fn_off[i];
@@ -458,6 +632,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
 
         // ---- result: pool sorted (score desc, id asc), first min(k, |pool|)
         {
+            if constexpr (MODE == 1) rescore(collect_pool([&](float) { return true; }), 0);
             const int np = st.nPool, pc = st.pool_cur;
             for (int i = tid; i < np; i += GR_NT) { sortk[i] = pkey[pc][i]; sortv[i] = pslot[pc][i]; }
             __syncthreads();
@@ -472,6 +647,12 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     a.out_scores[q * a.k + j] = __longlong_as_double(0x7ff8000000000000ll);
                 }
             }
+            if constexpr (MODE == 1) {
+                // hop at which the best item was scored (pool meta)
+                for (int i = tid; i < np; i += GR_NT)
+                    if (nr > 0 && pslot[pc][i] == sortv[0]) st.besthop = pmeta[pc][i] >> 1;
+                __syncthreads();
+            }
             if (tid == 0) {
                 a.out_count[q] = nr;
                 int64_t ev = 0;
@@ -483,5 +664,11 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 a.out_stats[q * nst + 4] = st.nbrs;
             }
         }
+    }
+    if constexpr (MODE == 1) {
+        tc::fence_before();
+        __syncthreads();
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
     }
 }

@@ -38,6 +38,10 @@ class SearchParams:
     ef: int | None = None
     deterministic: bool = True
     n_threads: int | None = None
+    # device-only extras (not in the reference): scoring engine and refinement band
+    mode: str = "exact"          # "exact": CUDA-core exact fp32 | "tc": tcgen05 + exact refinement
+    band_rel: float = 0.0        # <= 0: library default (1e-3)
+    band_abs: float = 0.0
 
     def __post_init__(self):
         if self.k < 1 or self.k_parallel < 1 or self.hops < 1:
@@ -46,13 +50,17 @@ class SearchParams:
             raise InvalidArgumentError("k_parallel must not exceed k")
         if self.ef is not None and self.ef < 1:
             raise InvalidArgumentError("ef must be >= 1")
+        if self.mode not in ("exact", "tc"):
+            raise InvalidArgumentError("mode must be 'exact' or 'tc'")
 
     @property
     def frontier_width(self) -> int:
         return self.ef if self.ef is not None else 2 * self.k
 
     def _c(self) -> _lib.SearchParamsC:
-        return _lib.SearchParamsC(self.k, self.k_parallel, self.hops, self.frontier_width)
+        return _lib.SearchParamsC(self.k, self.k_parallel, self.hops, self.frontier_width,
+                                  _lib.GR_MODE_TC if self.mode == "tc" else _lib.GR_MODE_EXACT,
+                                  self.band_rel, self.band_abs)
 
 
 @dataclass

@@ -187,3 +187,43 @@ def test_large_generated_graph_matches_c_oracle(P):
         np.testing.assert_array_equal(r.rows_expanded, o["rows"])
         np.testing.assert_array_equal(r.nbr_ids_read, o["nbr_ids"])
         np.testing.assert_array_equal(r.per_layer, o["per_layer"])
+
+
+@pytest.mark.parametrize("fixture", ["search_d64_z2", "search_d128_z3"])
+def test_tensor_core_mode_matches_reference(P, fixture):
+    """tcgen05 split-bf16 scoring + exact band refinement: same ids/scores/counts as exact."""
+    z = G.load(fixture)
+    metric = metric_of(P, z)
+    index = index_of(P, z)
+    for pi, p in G.param_sets(z):
+        r = P.c_hipanns_batch(index, metric, z["users"], z["emb"], P.SearchParams(**p, mode="tc"))
+        exp = G.expected(z, pi)
+        np.testing.assert_array_equal(r.ids, exp["ids"])
+        np.testing.assert_array_equal(r.scores, exp["scores"])
+        np.testing.assert_array_equal(r.evals, exp["evals"])
+        np.testing.assert_array_equal(r.per_layer, exp["per_layer"])
+        np.testing.assert_array_equal(r.hops_to_best, exp["best_hop"])
+
+
+def test_tensor_core_mode_large_graph_equals_exact(P):
+    from paper_2502_11490_b200 import _lib
+
+    rng = np.random.default_rng(12)
+    n, d = 60_000, 128
+    model = P.create_model(d_x=d, d_h=d, z_dim=3, hidden=(64, 64), seed=1)
+    centers = rng.normal(scale=4.0, size=(256, d))
+    feats = (centers[rng.integers(0, 256, size=n)] + rng.normal(size=(n, d))).astype(np.float32)
+    emb = model.item_embeddings(feats).astype(np.float32)
+    index = P.GraphIndex.build(emb, m=16, seed=0)
+    users = model.user_embedding(rng.normal(size=(200, d)).astype(np.float32)).astype(np.float32)
+    s = _lib.DeviceSearcher(0)
+    for kw in (dict(k=100, k_parallel=8, hops=3, ef=200), dict(k=50, k_parallel=16, hops=5, ef=40)):
+        ex = P.c_hipanns_batch(index, model, users, emb, P.SearchParams(**kw))
+        tc = P.c_hipanns_batch(index, model, users, emb, P.SearchParams(**kw, mode="tc"), searcher=s)
+        np.testing.assert_array_equal(tc.ids, ex.ids)
+        np.testing.assert_array_equal(tc.scores, ex.scores)
+        np.testing.assert_array_equal(tc.evals, ex.evals)
+        np.testing.assert_array_equal(tc.hops_to_best, ex.hops_to_best)
+    c = s.counters()
+    assert c["tensor_scored"] > 0
+    assert c["exact_rescored"] < 0.5 * c["tensor_scored"], c

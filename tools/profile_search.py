@@ -22,9 +22,13 @@ def main():
     nq = int(sys.argv[2]) if len(sys.argv) > 2 else 8192
     reps = int(sys.argv[3]) if len(sys.argv) > 3 else 3
     kw = dict(k=100, k_parallel=8, hops=3, ef=200)
-    if len(sys.argv) > 4:
+    if len(sys.argv) > 4 and sys.argv[4] != "-":
         kp, hops = (int(v) for v in sys.argv[4].split("x"))
         kw.update(k_parallel=kp, hops=hops)
+    if len(sys.argv) > 5:
+        kw["mode"] = sys.argv[5]
+    if os.environ.get("BAND"):
+        kw["band_rel"] = kw["band_abs"] = float(os.environ["BAND"])
     torch.cuda.set_device(0)
     wl = workload.make(cfg, n_queries=nq)
     dm = wl.model.metric.device_model(0)
@@ -50,6 +54,7 @@ def main():
         stats = ost.cpu().numpy()
         print(f"launch {r}: {dt*1e3:.2f} ms  {Q/dt:.0f} q/s  evals/q {stats[:,0].mean():.1f} "
               f"rows/q {stats[:,3].mean():.1f} nbrs/q {stats[:,4].mean():.1f}", flush=True)
+    print("counters", s.counters(), flush=True)
 
 
 if __name__ == "__main__":
