@@ -131,7 +131,10 @@ int gr_searcher_status(gr_searcher *s, void *stream);
 /* kernel launches issued by this searcher so far (evidence counter for bench.py) */
 int64_t gr_searcher_launches(const gr_searcher *s);
 /* cumulative scoring counters of this searcher: out[0] = exact re-scores (tensor-core
- * mode), out[1] = tensor-core scores.  Synchronises the device. */
+ * mode), out[1] = tensor-core scores; when the searcher was created with
+ * GMPGR_PHASE_TIMING=1 in the environment, out[2..9] = summed SM cycles per search phase
+ * (init, seeds, expand, resolve, score, pool, frontier, output).  out must hold 10 values.
+ * Synchronises the device. */
 int gr_searcher_counters(gr_searcher *s, int64_t *out);
 
 /* Exact top-k over ALL items of the handle for Q users (ground truth, search.py:93-108):

@@ -232,6 +232,11 @@ class DeviceSearcher(_Handle):
         return int(lib().gr_searcher_launches(self.h))
 
     def counters(self) -> dict:
-        out = np.zeros(2, dtype=np.int64)
+        out = np.zeros(10, dtype=np.int64)
         check(lib().gr_searcher_counters(self.h, ptr(out)))
-        return {"exact_rescored": int(out[0]), "tensor_scored": int(out[1])}
+        d = {"exact_rescored": int(out[0]), "tensor_scored": int(out[1])}
+        if out[2:].any():
+            names = ("init", "seeds", "expand", "resolve", "score", "pool", "frontier", "output")
+            tot = float(out[2:].sum())
+            d["phase_share"] = {k: round(float(v) / tot, 4) for k, v in zip(names, out[2:])}
+        return d

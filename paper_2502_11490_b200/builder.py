@@ -300,7 +300,7 @@ def merge_rows(r1, c1, r2, c2, cap: int):
 
 def build_layers(vectors, m: int = 16, level_prob: float = 1.0 / 17.0, max_layers: int = 4,
                  seed: int = 0, device=None, exact_limit: int = 200_000, long_frac: float = 0.0,
-                 n_random: int = 256, mode: str = "hnsw"):
+                 n_random: int = 64, mode: str = "hnsw"):
     """Return dict(levels, entry_slot, n_layers, nbrs=[(n, cap_l) int32], cnts=[(n,) int32])."""
     torch = _torch()
     dev = torch.device(device if device is not None else "cuda")

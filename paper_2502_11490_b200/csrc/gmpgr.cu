@@ -6,6 +6,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <string>
@@ -127,6 +128,7 @@ struct gr_searcher {
     uint64_t *fr_key = nullptr, *seg_key = nullptr, *pool_key = nullptr;
     int32_t *pool_meta = nullptr;
     unsigned long long *counters = nullptr;
+    unsigned long long *phase = nullptr; // [8] when GMPGR_PHASE_TIMING=1
     int *flags = nullptr; // [0] queue, [1] nonfinite, [2] bad index
     int64_t launches = 0;
     // staging for host-pointer calls
@@ -559,6 +561,8 @@ template <class K>
 int set_smem(K kernel, int bytes) {
     if (bytes > kMaxSmem) return fail(GR_EINVAL, "model too large for shared memory");
     GR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+    // prefer the largest shared-memory carveout so two ~100 KB CTAs co-reside per SM
+    GR_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributePreferredSharedMemoryCarveout, 100));
     return GR_OK;
 }
 
@@ -688,6 +692,7 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     a.pool_slot = S->pool_slot;
     a.pool_meta = S->pool_meta;
     a.counters = S->counters;
+    a.phase_cycles = S->phase;
     a.band_rel = p->band_rel > 0.f ? p->band_rel : 1e-3f;
     a.band_abs = p->band_abs > 0.f ? p->band_abs : 1e-3f;
     a.capF = S->capF;
@@ -715,6 +720,10 @@ int gr_searcher_create(int device, gr_searcher **out) {
     cudaMemset(S->flags, 0, 16);
     if (int rc = dmalloc(&S->counters, 2)) { cudaFree(S->flags); delete S; return rc; }
     cudaMemset(S->counters, 0, 16);
+    const char *pt = getenv("GMPGR_PHASE_TIMING");
+    if (pt && pt[0] == '1') {
+        if (dmalloc(&S->phase, 8) == GR_OK) cudaMemset(S->phase, 0, 64);
+    }
     *out = S;
     return GR_OK;
 }
@@ -725,6 +734,7 @@ int gr_searcher_destroy(gr_searcher *s) {
     s->free_scratch();
     cudaFree(s->flags);
     cudaFree(s->counters);
+    if (s->phase) cudaFree(s->phase);
     s->st_users.release();
     s->st_ids.release();
     s->st_scores.release();
@@ -741,6 +751,7 @@ int gr_searcher_counters(gr_searcher *s, int64_t *out) {
     GR_CUDA(cudaSetDevice(s->device));
     GR_CUDA(cudaDeviceSynchronize());
     GR_CUDA(cudaMemcpy(out, s->counters, 16, cudaMemcpyDeviceToHost));
+    if (s->phase) GR_CUDA(cudaMemcpy(out + 2, s->phase, 64, cudaMemcpyDeviceToHost));
     return GR_OK;
 }
 

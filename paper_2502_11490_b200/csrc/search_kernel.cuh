@@ -51,6 +51,7 @@ struct SearchArgs {
     int32_t *pool_meta; // [slots][2][capP]: eval hop << 1 | exact (tensor-core mode)
     unsigned long long *counters; // [0] exact re-scores, [1] tensor-core scores
     float band_rel, band_abs;     // refinement band: |s - T| <= band_rel*|T| + band_abs
+    unsigned long long *phase_cycles; // nullable: per-phase SM cycles (instrumentation)
     int64_t capF, capS, capP;
     int *queue;
     int *nonfinite;
@@ -104,8 +105,20 @@ template <int MINB, int DH, int ZZ, int MODE>
 __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const SearchArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CtaState st;
+    __shared__ unsigned long long ph_acc[8];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const DevModel &M = a.M;
+    // phase timing (thread 0, after the barrier that closes each phase)
+    long long ph_t0 = 0;
+    if (tid < 8) ph_acc[tid] = 0;
+#define GR_PH(i)                                                          \
+    do {                                                                  \
+        if (a.phase_cycles && tid == 0) {                                 \
+            const long long now_ = clock64();                             \
+            ph_acc[i] += (unsigned long long)(now_ - ph_t0);              \
+            ph_t0 = now_;                                                 \
+        }                                                                 \
+    } while (0)
     const DevGraph &g = a.g;
 
     // ---- carve shared memory, load weights once per CTA
@@ -227,6 +240,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         __syncthreads();
         const int64_t q = st.q;
         if (q >= a.Q) break;
+        if (tid == 0) ph_t0 = clock64();
         const uint32_t epoch = st.epoch;
         const float *hu = a.users + q * d_h;
 
@@ -480,6 +494,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
             score_fresh(nFresh, 0);
             after_score(top, 0, nFresh);
         }
+        GR_PH(0);
 
         int h = 0;
         for (int layer = top; layer >= 0; --layer) {
@@ -507,6 +522,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 if (tid == 0) { st.nF = ns; st.f_cur = 0; }
                 __syncthreads();
             }
+            GR_PH(1);
             const int deg = g.deg[layer];
             for (int t = 0; t < a.hops; ++t) {
                 ++h;
@@ -553,10 +569,14 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     }
                 }
                 __syncthreads();
+                GR_PH(2);
                 resolve(st.nS, 0);
+                GR_PH(3);
                 const int nFresh = st.nFresh;
                 score_fresh(nFresh, h);
+                GR_PH(4);
                 after_score(layer, h, nFresh);
+                GR_PH(5);
                 if (t == a.hops - 1) break; // frontier after a layer's last hop is unused
                 // ---- per-searcher top-ef of fresh claims -> next frontier
                 const int nsr = a.kp;
@@ -627,6 +647,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 __syncthreads();
                 if (tid == 0) { st.nF = st.nFn; st.f_cur = fn; }
                 __syncthreads();
+                GR_PH(6);
             }
         }
 
@@ -664,7 +685,10 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 a.out_stats[q * nst + 4] = st.nbrs;
             }
         }
+        GR_PH(7);
     }
+    if (a.phase_cycles && tid < 8) atomicAdd(a.phase_cycles + tid, ph_acc[tid]);
+#undef GR_PH
     if constexpr (MODE == 1) {
         tc::fence_before();
         __syncthreads();

@@ -68,6 +68,7 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     del centers, assign
     index = GraphIndex.build(items, m=m, seed=0, device=dev)
     torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()  # hand the builder's cached blocks back before the search scratch
     items_host = items.cpu().numpy() if host_items else None
     return Workload(name, model, items, items_host, np.ascontiguousarray(users, np.float32), index,
                     time.perf_counter() - t0)
