@@ -16,6 +16,7 @@
 #include "aux_kernels.cuh"
 #include "common.cuh"
 #include "search_kernel.cuh"
+#include "search_mq.cuh"
 
 namespace {
 
@@ -624,6 +625,99 @@ int check_params(const gr_search_params *p) {
     return GR_OK;
 }
 
+template <int DH, int ZZ, int MODE>
+int plan_mq(int k, int kp, SearchArgs &a) {
+    using EX = ExactQ<DH, ZZ>;
+    using TC = TcQ<DH, ZZ>;
+    SmemPlan P;
+    a.off_w0 = P.alloc(EX::W_END * 16);
+    a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, TC::A_BYTES));
+    a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
+    a.off_acc0 = P.alloc(mq::G * 64 * 16);
+    a.off_hist = P.alloc(mq::NW * 256 * 4);
+    a.sortcap = pow2ceil(std::max(k, kp));
+    a.off_sortk = P.alloc(mq::G * a.sortcap * 8);
+    a.off_sortv = P.alloc(mq::G * a.sortcap * 4);
+    a.off_kp = P.alloc(3 * mq::G * kp * 4);
+    return P.bytes;
+}
+
+// multi-query kernel for the fixed model shapes (search_mq.cuh); returns -1 if not applicable
+int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I,
+              const float *users, int64_t Q, const gr_search_params *p, int64_t *ids,
+              double *scores, int32_t *count, int64_t *stats, cudaStream_t stream, int shape) {
+    SearchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    const int mode = p->mode;
+    int smem = 0;
+    void (*kern)(const SearchArgs) = nullptr;
+#define GR_MQ_CASE(CODE, DH, ZZ)                                                        \
+    case CODE:                                                                          \
+        if (mode == GR_MODE_TC) { smem = plan_mq<DH, ZZ, 1>(p->k, p->k_parallel, a); kern = hipanns_mq_kernel<DH, ZZ, 1>; } \
+        else { smem = plan_mq<DH, ZZ, 0>(p->k, p->k_parallel, a); kern = hipanns_mq_kernel<DH, ZZ, 0>; } \
+        break;
+    switch (shape) {
+        GR_MQ_CASE(1283, 128, 3)
+        GR_MQ_CASE(1282, 128, 2)
+        GR_MQ_CASE(643, 64, 3)
+        GR_MQ_CASE(642, 64, 2)
+    default: return -1;
+    }
+#undef GR_MQ_CASE
+    if (smem > kMaxSmem) return -1;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 0;
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, mq::NT, smem));
+    if (per_sm < 1) return -1;
+    const int64_t blocks = std::min<int64_t>((Q + mq::G - 1) / mq::G, (int64_t)per_sm * num_sms(G->device));
+    const int64_t capF = (int64_t)p->k_parallel * p->ef;
+    int64_t capS = std::min<int64_t>(capF * G->max_deg, (int64_t)p->k_parallel * G->dg.n);
+    capS = std::max<int64_t>(capS, G->max_deg + 1) + 64;
+    const int64_t capP = p->k + capS;
+    if (int rc = ensure_search_scratch(S, G, blocks * mq::G, capF, capS, capP)) return rc;
+    a.g = G->dg;
+    a.M = M->dm;
+    a.it = I->di;
+    a.users = users;
+    a.Q = Q;
+    a.k = p->k;
+    a.kp = p->k_parallel;
+    a.hops = p->hops;
+    a.ef = p->ef;
+    a.out_ids = ids;
+    a.out_scores = scores;
+    a.out_count = count;
+    a.out_stats = stats;
+    a.tags = S->tags;
+    a.epochs = S->epochs;
+    a.f_slot = S->f_slot;
+    a.f_srch = S->f_srch;
+    a.surv_v = S->surv_v;
+    a.surv_i = S->surv_i;
+    a.fr_v = S->fr_v;
+    a.fr_i = S->fr_i;
+    a.fr_key = S->fr_key;
+    a.seg_v = S->seg_v;
+    a.seg_key = S->seg_key;
+    a.pool_key = S->pool_key;
+    a.pool_slot = S->pool_slot;
+    a.pool_meta = S->pool_meta;
+    a.counters = S->counters;
+    a.phase_cycles = S->phase;
+    a.band_rel = p->band_rel > 0.f ? p->band_rel : 1e-3f;
+    a.band_abs = p->band_abs > 0.f ? p->band_abs : 1e-3f;
+    a.capF = S->capF * mq::G;  // CTA-level flattened lists
+    a.capS = S->capS * mq::G;
+    a.capP = S->capP;          // per-query pools
+    a.queue = S->flags;
+    a.nonfinite = S->flags + 1;
+    GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
+    kern<<<(int)blocks, mq::NT, smem, stream>>>(a);
+    GR_CUDA(cudaGetLastError());
+    S->launches += 1;
+    return GR_OK;
+}
+
 int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I,
                   const float *users, int64_t Q, const gr_search_params *p, int64_t *ids,
                   double *scores, int32_t *count, int64_t *stats, cudaStream_t stream) {
@@ -634,6 +728,12 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     const int mode = p->mode;
     if (mode == GR_MODE_TC && (!shape || !M->dm.tc_ok))
         return fail(GR_EINVAL, "tensor-core mode needs the (d_h in {64,128}, hidden (64,64), Z in {2,3}) model shape");
+    // fixed shapes run the multi-query kernel unless GMPGR_KERNEL=cta selects the per-query one
+    const char *kenv = getenv("GMPGR_KERNEL");
+    if (shape && !(kenv && std::strcmp(kenv, "cta") == 0)) {
+        const int rc = launch_mq(S, G, M, I, users, Q, p, ids, scores, count, stats, stream, shape);
+        if (rc != -1) return rc;
+    }
     const int smem = plan_search(M->dm, p->k, p->k_parallel, a, shape, mode);
     void (*kern)(const SearchArgs) = nullptr;
     if (mode == GR_MODE_TC) {

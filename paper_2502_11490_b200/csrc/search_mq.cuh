@@ -1,0 +1,873 @@
+// Multi-query persistent C-HiPANNS kernel: one 512-thread CTA per SM advances G = 4
+// queries in lock-step (same layers, same hops), so every phase works on 4 queries'
+// frontiers / claims / fresh sets at once — more independent memory traffic in flight,
+// fuller scoring tiles, one copy of the weights per SM.  Semantics are exactly those of
+// search_kernel.cuh (hop-synchronous c_hipanns, search.py:194-286): each query owns its
+// own epoch-stamped tag array, pool and frontier; flattened work lists carry the query
+// slot g in the high half of the searcher field (g << 16 | searcher).
+//
+// MODE 0: exact-fp32 scoring of every claim (64-pair tiles, weights in shared memory).
+// MODE 1: tcgen05 split-bf16 scoring of 128-pair tiles + exact re-scoring of the band
+//         around every selection threshold (see search_kernel.cuh for the argument).
+#pragma once
+#include "common.cuh"
+#include "mlp_exact.cuh"
+#include "search_kernel.cuh"
+#include "select.cuh"
+#include "tc_scorer.cuh"
+
+namespace mq {
+constexpr int NT = 512, NW = NT / 32, G = 4, GT = NT / G; // group threads for per-query sorts
+constexpr int PT = 4 * NW;                                   // exact tile: 64 pairs
+}  // namespace mq
+
+// Exact fixed-shape MLP on 64-pair tiles whose pairs may belong to different queries
+// (per-pair hoisted user half acc0[g]).  Same arithmetic as FixedMlp (bit-exact order).
+template <int D_H, int Z>
+struct ExactQ {
+    static constexpr int H = 64, NCH0 = D_H / 4, NCHH = H / 4, NCHZ = (Z + 3) / 4;
+    static constexpr int LDX0 = NCH0 | 1, LDH = NCHH | 1, LDZ = NCHZ | 1, PT = mq::PT;
+    // float4 offsets of the weight block (same layout as FixedMlp) ...
+    static constexpr int OFF_W0 = 0;
+    static constexpr int OFF_W1 = OFF_W0 + NCH0 * H;
+    static constexpr int OFF_W2 = OFF_W1 + NCHH * H;
+    static constexpr int OFF_A = OFF_W2 + NCHH * Z;
+    static constexpr int OFF_B0 = OFF_A + NCHZ;
+    static constexpr int OFF_B1 = OFF_B0 + H / 4;
+    static constexpr int OFF_B2 = OFF_B1 + H / 4;
+    static constexpr int W_END = OFF_B2 + NCHZ;
+    // ... and of the activation buffers (relative to their own base)
+    static constexpr int OFF_X0 = 0;
+    static constexpr int OFF_H0 = OFF_X0 + PT * LDX0;
+    static constexpr int OFF_H1 = OFF_H0 + PT * LDH;
+    static constexpr int OFF_Z = OFF_H1 + PT * LDH;
+    static constexpr int OFF_SC = OFF_Z + PT * LDZ;
+    static constexpr int OFF_PQ = OFF_SC + PT / 4;
+    static constexpr int BUF_END = OFF_PQ + PT / 4;
+
+    template <int NCH, int LDX, bool HAS_INIT>
+    static __device__ __forceinline__ void big(const float4 *__restrict__ X,
+                                               const float4 *__restrict__ W,
+                                               const float *__restrict__ bias,
+                                               const float4 *__restrict__ acc0,
+                                               const int *__restrict__ pq, float *__restrict__ Y) {
+        const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+        float4 a[4][2];
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            if (HAS_INIT) {
+                const int g = pq[warp * 4 + pp];
+                a[pp][0] = acc0[g * H + lane];
+                a[pp][1] = acc0[g * H + lane + 32];
+            } else {
+                a[pp][0] = make_float4(0.f, 0.f, 0.f, 0.f);
+                a[pp][1] = a[pp][0];
+            }
+        }
+        const float4 *xr = X + warp * 4 * LDX;
+        const float4 *wr = W + lane;
+#pragma unroll 8
+        for (int j = 0; j < NCH; ++j) {
+            const float4 w0 = wr[j * H], w1 = wr[j * H + 32];
+#pragma unroll
+            for (int pp = 0; pp < 4; ++pp) {
+                const float4 x = xr[pp * LDX + j];
+                mac4(a[pp][0], x, w0);
+                mac4(a[pp][1], x, w1);
+            }
+        }
+        const float b0 = bias[lane], b1 = bias[lane + 32];
+        const int j0 = chunk_perm(lane >> 2, H) * 4 + (lane & 3);
+        const int j1 = chunk_perm((lane + 32) >> 2, H) * 4 + (lane & 3);
+#pragma unroll
+        for (int pp = 0; pp < 4; ++pp) {
+            const int p = warp * 4 + pp;
+            Y[p * LDH * 4 + j0] = relu_np(__fadd_rn(hsum4(a[pp][0]), b0));
+            Y[p * LDH * 4 + j1] = relu_np(__fadd_rn(hsum4(a[pp][1]), b1));
+        }
+    }
+
+    // W: weight block (smem); buf: activation buffers (smem); acc0: [G][64] float4
+    static __device__ __forceinline__ void tile(const float4 *W, float4 *buf, const float4 *acc0,
+                                                int n_valid, int *nonfinite) {
+        const int *pq = reinterpret_cast<const int *>(buf + OFF_PQ);
+        big<NCH0, LDX0, true>(buf + OFF_X0, W + OFF_W0, reinterpret_cast<const float *>(W + OFF_B0),
+                              acc0, pq, reinterpret_cast<float *>(buf + OFF_H0));
+        __syncthreads();
+        big<NCHH, LDH, false>(buf + OFF_H0, W + OFF_W1, reinterpret_cast<const float *>(W + OFF_B1),
+                              nullptr, pq, reinterpret_cast<float *>(buf + OFF_H1));
+        __syncthreads();
+        float *zb = reinterpret_cast<float *>(buf + OFF_Z);
+        if (threadIdx.x < PT * Z) {
+            const int p = threadIdx.x % PT, o = threadIdx.x / PT;
+            const float4 *hr = buf + OFF_H1 + p * LDH;
+            const float4 *W2 = W + OFF_W2;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < NCHH; ++j) mac4(acc, hr[j], W2[j * Z + o]);
+            zb[p * LDZ * 4 + o] =
+                __fadd_rn(hsum4(acc), reinterpret_cast<const float *>(W + OFF_B2)[o]);
+        }
+        __syncthreads();
+        if (threadIdx.x < PT) {
+            const int p = threadIdx.x;
+            const float *z = zb + p * LDZ * 4;
+            bool bad = false;
+#pragma unroll
+            for (int o = 0; o < Z; ++o) bad |= !isfinite(z[o]);
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+            for (int j = 0; j < NCHZ; ++j) {
+                const int c = chunk_perm(j, Z);
+                float e[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) e[u] = (4 * c + u < Z) ? z[4 * c + u] : 0.f;
+                mac4(acc, make_float4(e[0], e[1], e[2], e[3]), W[OFF_A + j]);
+            }
+            reinterpret_cast<float *>(buf + OFF_SC)[p] = hsum4(acc);
+            if (bad && p < n_valid) atomicOr(nonfinite, 1);
+        }
+        __syncthreads();
+    }
+};
+
+// tcgen05 scorer for 512-thread CTAs: 128-pair tiles, per-pair query user half.
+template <int D_H, int Z>
+struct TcQ {
+    static constexpr int H = 64, TM = 128, KC = 64, NKC0 = D_H / KC;
+    static constexpr int OFF_B0H = 0;
+    static constexpr int OFF_B0L = OFF_B0H + H * D_H * 2;
+    static constexpr int OFF_B1H = OFF_B0L + H * D_H * 2;
+    static constexpr int OFF_B1L = OFF_B1H + H * H * 2;
+    static constexpr int A_BYTES = 2 * TM * KC * 2;       // A operand (hi, lo): caller-provided
+    static constexpr int OFF_U = OFF_B1L + H * H * 2;     // [G][64] f32 user half + b0
+    static constexpr int OFF_B1 = OFF_U + mq::G * H * 4;
+    static constexpr int OFF_W2 = OFF_B1 + H * 4;         // [Z][64]
+    static constexpr int OFF_B2 = OFF_W2 + Z * H * 4;
+    static constexpr int OFF_ATT = OFF_B2 + 16;
+    static constexpr int OFF_ZP = OFF_ATT + 16;           // [128][4][Z]
+    static constexpr int OFF_SC = OFF_ZP + TM * 4 * Z * 4;
+    static constexpr int OFF_PQ = OFF_SC + TM * 4;        // [128] query slot per row
+    static constexpr int OFF_BAR = (OFF_PQ + TM * 4 + 15) & ~15;
+    static constexpr int OFF_TMEM = OFF_BAR + 16;
+    static constexpr int BYTES = OFF_TMEM + 16;
+    static constexpr uint32_t IDESC = tc::idesc(TM, H);
+
+    static __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+        uint32_t r[16];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),
+              "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(addr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;");
+#pragma unroll
+        for (int j = 0; j < 16; ++j) v[j] = __uint_as_float(r[j]);
+    }
+
+    // rows: slots[0..nv), query slot per row in PQ (written by the caller)
+    static __device__ __forceinline__ void tile(unsigned char *sm, unsigned char *abuf, uint32_t tmem,
+                                                uint32_t &phase, const DevItems &it,
+                                                const DevGraph &g, const int32_t *slots, int nv) {
+        const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        unsigned char *Ah = abuf, *Al = abuf + TM * KC * 2;
+        uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
+        const uint32_t aH = tc::smem_u32(Ah), aL = tc::smem_u32(Al);
+        for (int kc = 0; kc < NKC0; ++kc) {
+            for (int t = tid; t < TM * 16; t += mq::NT) {
+                const int r = t >> 4, c = t & 15;
+                if (r < nv) {
+                    const float4 x = __ldg(reinterpret_cast<const float4 *>(
+                                               it.emb + slot_row(g, slots[r]) * it.ld) + kc * 16 + c);
+                    uint2 hi, lo;
+                    tc::split4(x, hi, lo);
+                    const uint32_t off = tc::kmaj_off(r, 4 * c, KC);
+                    *reinterpret_cast<uint2 *>(Ah + off) = hi;
+                    *reinterpret_cast<uint2 *>(Al + off) = lo;
+                }
+            }
+            tc::fence_async_smem();
+            tc::fence_before();
+            __syncthreads();
+            if (tid == 0) {
+                tc::fence_after();
+                const uint32_t bH = tc::smem_u32(sm + OFF_B0H), bL = tc::smem_u32(sm + OFF_B0L);
+#pragma unroll
+                for (int k = 0; k < KC / 16; ++k) {
+                    const uint64_t ah = tc::desc(aH + k * 256, KC), al = tc::desc(aL + k * 256, KC);
+                    const uint32_t kb = (kc * (KC / 16) + k) * 256;
+                    const uint64_t bh = tc::desc(bH + kb, D_H), bl = tc::desc(bL + kb, D_H);
+                    tc::mma(tmem, ah, bh, IDESC, (kc | k) ? 1u : 0u);
+                    tc::mma(tmem, ah, bl, IDESC, 1u);
+                    tc::mma(tmem, al, bh, IDESC, 1u);
+                }
+                tc::commit(bar);
+            }
+            tc::mbar_wait(bar, phase);
+            phase ^= 1u;
+            tc::fence_after();
+        }
+        const int q4 = warp & 3, cq = warp >> 2, row = q4 * 32 + lane;
+        const int gq = reinterpret_cast<const int *>(sm + OFF_PQ)[row];
+        const float *u = reinterpret_cast<const float *>(sm + OFF_U) + gq * H;
+        {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + cq * 16, v);
+#pragma unroll
+            for (int j = 0; j < 16; j += 4) {
+                const int o = cq * 16 + j;
+                float4 y = make_float4(fmaxf(v[j] + u[o], 0.f), fmaxf(v[j + 1] + u[o + 1], 0.f),
+                                       fmaxf(v[j + 2] + u[o + 2], 0.f), fmaxf(v[j + 3] + u[o + 3], 0.f));
+                uint2 hi, lo;
+                tc::split4(y, hi, lo);
+                const uint32_t off = tc::kmaj_off(row, o, H);
+                *reinterpret_cast<uint2 *>(Ah + off) = hi;
+                *reinterpret_cast<uint2 *>(Al + off) = lo;
+            }
+        }
+        tc::fence_async_smem();
+        tc::fence_before();
+        __syncthreads();
+        if (tid == 0) {
+            tc::fence_after();
+            const uint32_t bH = tc::smem_u32(sm + OFF_B1H), bL = tc::smem_u32(sm + OFF_B1L);
+#pragma unroll
+            for (int k = 0; k < H / 16; ++k) {
+                const uint64_t ah = tc::desc(aH + k * 256, H), al = tc::desc(aL + k * 256, H);
+                const uint64_t bh = tc::desc(bH + k * 256, H), bl = tc::desc(bL + k * 256, H);
+                tc::mma(tmem + 64, ah, bh, IDESC, k ? 1u : 0u);
+                tc::mma(tmem + 64, ah, bl, IDESC, 1u);
+                tc::mma(tmem + 64, al, bh, IDESC, 1u);
+            }
+            tc::commit(bar);
+        }
+        tc::mbar_wait(bar, phase);
+        phase ^= 1u;
+        tc::fence_after();
+        {
+            float v[16];
+            tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + 64 + cq * 16, v);
+            const float *b1 = reinterpret_cast<const float *>(sm + OFF_B1);
+            const float *W2 = reinterpret_cast<const float *>(sm + OFF_W2);
+            float zp[Z];
+#pragma unroll
+            for (int o = 0; o < Z; ++o) zp[o] = 0.f;
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const float h = fmaxf(v[j] + b1[cq * 16 + j], 0.f);
+#pragma unroll
+                for (int o = 0; o < Z; ++o) zp[o] = fmaf(h, W2[o * H + cq * 16 + j], zp[o]);
+            }
+            float *ZP = reinterpret_cast<float *>(sm + OFF_ZP);
+#pragma unroll
+            for (int o = 0; o < Z; ++o) ZP[(row * 4 + cq) * Z + o] = zp[o];
+        }
+        tc::fence_before();
+        __syncthreads();
+        if (tid < TM) {
+            const float *ZP = reinterpret_cast<const float *>(sm + OFF_ZP);
+            const float *b2 = reinterpret_cast<const float *>(sm + OFF_B2);
+            const float *att = reinterpret_cast<const float *>(sm + OFF_ATT);
+            float s = 0.f;
+#pragma unroll
+            for (int o = 0; o < Z; ++o) {
+                const float z = ((ZP[(tid * 4) * Z + o] + ZP[(tid * 4 + 1) * Z + o]) +
+                                 (ZP[(tid * 4 + 2) * Z + o] + ZP[(tid * 4 + 3) * Z + o])) + b2[o];
+                s = fmaf(z, att[o], s);
+            }
+            reinterpret_cast<float *>(sm + OFF_SC)[tid] = s;
+        }
+        __syncthreads();
+    }
+};
+
+struct MqQuery {
+    int q;             // global query index, -1 if this slot is idle
+    uint32_t epoch;
+    int nPool, nPool2, pool_cur, f_off, f_cnt;
+    uint64_t poolT;
+    int besthop;
+    int64_t per_layer[GR_MAX_LAYERS];
+    int64_t rows, nbrs;
+};
+
+struct MqState {
+    MqQuery qs[mq::G];
+    int nF, nS, nFresh, nFn, nRq, f_cur, base;
+    uint32_t bcast[4];
+};
+
+// Shared-memory plan (host computes the same offsets): [model block][exact buffers]
+// [hist NW x 256][sort G x sortcap keys+vals][seg cnt/off/fn: 3 x G*kp][acc0 G x 64 float4]
+template <int DH, int ZZ, int MODE>
+__global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs a) {
+    using EX = ExactQ<DH, ZZ>;
+    using TC = TcQ<DH, ZZ>;
+    constexpr int G = mq::G, NT = mq::NT, NW = mq::NW;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    __shared__ MqState st;
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const DevModel &M = a.M;
+    const DevGraph &g = a.g;
+    // ---- shared memory carve (offsets from the host plan)
+    float4 *sW = reinterpret_cast<float4 *>(smem + a.off_w0);      // exact weight block
+    float4 *sBuf = reinterpret_cast<float4 *>(smem + a.off_x0);    // exact activation buffers
+    float4 *sAcc0 = reinterpret_cast<float4 *>(smem + a.off_acc0); // [G][64]
+    uint32_t *hist = reinterpret_cast<uint32_t *>(smem + a.off_hist);
+    uint64_t *sortk = reinterpret_cast<uint64_t *>(smem + a.off_sortk); // [G][sortcap]
+    int32_t *sortv = reinterpret_cast<int32_t *>(smem + a.off_sortv);
+    int32_t *seg_cnt = reinterpret_cast<int32_t *>(smem + a.off_kp);    // [G*kp]
+    const int NSEG = G * a.kp;
+    int32_t *seg_off = seg_cnt + NSEG;
+    int32_t *fn_off = seg_off + NSEG;
+    // ---- exact weights (both modes: the tensor-core mode re-scores near thresholds)
+    {
+        const int O0 = 64, pre = M.pre_ch;
+        for (int t = tid; t < EX::NCH0 * O0; t += NT) sW[EX::OFF_W0 + t] = M.W[0][pre * O0 + t];
+        for (int t = tid; t < EX::NCHH * 64; t += NT) sW[EX::OFF_W1 + t] = M.W[1][t];
+        for (int t = tid; t < EX::NCHH * ZZ; t += NT) sW[EX::OFF_W2 + t] = M.W[2][t];
+        for (int t = tid; t < EX::NCHZ; t += NT) sW[EX::OFF_A + t] = M.A[t];
+        float *b0 = reinterpret_cast<float *>(sW + EX::OFF_B0), *b1 = reinterpret_cast<float *>(sW + EX::OFF_B1),
+              *b2 = reinterpret_cast<float *>(sW + EX::OFF_B2);
+        for (int t = tid; t < 64; t += NT) { b0[t] = M.b[0][t]; b1[t] = M.b[1][t]; }
+        for (int t = tid; t < 4 * EX::NCHZ; t += NT) b2[t] = t < ZZ ? M.b[2][t] : 0.f;
+    }
+    uint32_t tmem = 0, tphase = 0;
+    unsigned char *tcs = smem + a.off_A; // tensor-core block (MODE 1)
+    if constexpr (MODE == 1) {
+        const uint4 *src = reinterpret_cast<const uint4 *>(M.tcB);
+        uint4 *dst = reinterpret_cast<uint4 *>(tcs + TC::OFF_B0H);
+        for (int t = tid; t < (TC::OFF_U - TC::OFF_B0H) / 16; t += NT) dst[t] = src[t];
+        float *b1 = reinterpret_cast<float *>(tcs + TC::OFF_B1);
+        for (int t = tid; t < 64; t += NT) b1[t] = M.tcMisc[t];
+        float *w2 = reinterpret_cast<float *>(tcs + TC::OFF_W2);
+        for (int t = tid; t < 64 * ZZ; t += NT) w2[t] = M.tcMisc[64 + t];
+        if (tid < 4) {
+            reinterpret_cast<float *>(tcs + TC::OFF_B2)[tid] = M.tcMisc[64 + 64 * ZZ + tid];
+            reinterpret_cast<float *>(tcs + TC::OFF_ATT)[tid] = M.tcMisc[68 + 64 * ZZ + tid];
+        }
+        uint32_t *tptr = reinterpret_cast<uint32_t *>(tcs + TC::OFF_TMEM);
+        if (warp == 0) {
+            asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                             tc::smem_u32(tptr)), "r"(128));
+            asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+        }
+        if (tid == 0) tc::mbar_init(reinterpret_cast<uint64_t *>(tcs + TC::OFF_BAR), 1);
+        tc::fence_before();
+        __syncthreads();
+        tc::fence_after();
+        tmem = *tptr;
+    }
+    // ---- scratch: CTA-level flattened lists (capacities x G), per-query tags and pools
+    const int64_t cta = blockIdx.x;
+    const int64_t capF = a.capF, capS = a.capS, capP = a.capP; // already multiplied by G for lists
+    int32_t *fslot[2] = {a.f_slot + cta * 2 * capF, a.f_slot + cta * 2 * capF + capF};
+    int32_t *fsrch[2] = {a.f_srch + cta * 2 * capF, a.f_srch + cta * 2 * capF + capF};
+    int32_t *surv_v = a.surv_v + cta * capS, *surv_i = a.surv_i + cta * capS;
+    int32_t *fr_v = a.fr_v + cta * capS, *fr_i = a.fr_i + cta * capS;
+    uint64_t *fr_key = a.fr_key + cta * capS;
+    int32_t *seg_v = a.seg_v + cta * capS;
+    uint64_t *seg_key = a.seg_key + cta * capS;
+    int32_t *rq = surv_v;     // re-score requests (index | target bit 31)
+    int32_t *seg_ex = fr_i;   // after the scatter
+    auto tags_of = [&](int gq) { return a.tags + (cta * G + gq) * g.n; };
+    auto pkey = [&](int gq, int c) { return a.pool_key + ((cta * G + gq) * 2 + c) * capP; };
+    auto pslot = [&](int gq, int c) { return a.pool_slot + ((cta * G + gq) * 2 + c) * capP; };
+    auto pmeta = [&](int gq, int c) { return a.pool_meta + ((cta * G + gq) * 2 + c) * capP; };
+    auto band_of = [&](float T) { return a.band_rel * fabsf(T) + a.band_abs; };
+    const int top = g.n_layers - 1, nst = 5 + g.n_layers, d_h = DH;
+
+    for (;;) {
+        __syncthreads();
+        if (tid == 0) st.base = atomicAdd(a.queue, G);
+        __syncthreads();
+        if (st.base >= a.Q) break;
+        if (tid < G) {
+            MqQuery &Q = st.qs[tid];
+            Q.q = st.base + tid < a.Q ? st.base + tid : -1;
+            if (Q.q >= 0) {
+                const uint32_t e = a.epochs[cta * G + tid] + 1u;
+                a.epochs[cta * G + tid] = e;
+                Q.epoch = e;
+            }
+            Q.nPool = 0; Q.pool_cur = 0; Q.poolT = 0ull; Q.besthop = -1;
+            for (int l = 0; l < GR_MAX_LAYERS; ++l) Q.per_layer[l] = 0;
+            Q.rows = 0; Q.nbrs = 0;
+        }
+        if (tid == 0) { st.f_cur = 0; }
+        __syncthreads();
+        // ---- hoisted user halves (exact acc0; tensor-core u = user half + b0)
+        for (int t = tid; t < G * 64; t += NT) {
+            const int gq = t >> 6, o = t & 63;
+            const int q = st.qs[gq].q;
+            float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (q >= 0) {
+                const float *hu = a.users + (int64_t)q * d_h;
+                for (int j = 0; j < M.pre_ch; ++j) {
+                    const int c = chunk_perm(j, 2 * d_h);
+                    mac4(acc, make_float4(hu[4 * c], hu[4 * c + 1], hu[4 * c + 2], hu[4 * c + 3]),
+                         M.W[0][j * 64 + o]);
+                }
+            }
+            sAcc0[gq * 64 + o] = acc;
+            if constexpr (MODE == 1)
+                reinterpret_cast<float *>(tcs + TC::OFF_U)[gq * 64 + o] = __fadd_rn(hsum4(acc), M.b[0][o]);
+        }
+
+        // ================= helpers
+        // score fresh (fr_v, fr_i) [0, n): keys; per-query per-layer counts; pool append
+        auto score_fresh = [&](int n, int layer, int hop) {
+            if constexpr (MODE == 1) {
+                const float *sc = reinterpret_cast<const float *>(tcs + TC::OFF_SC);
+                int *pq = reinterpret_cast<int *>(tcs + TC::OFF_PQ);
+                for (int base = 0; base < n; base += TC::TM) {
+                    const int nv = min(TC::TM, n - base);
+                    if (tid < TC::TM) pq[tid] = tid < nv ? (fr_i[base + tid] >> 16) : 0;
+                    __syncthreads();
+                    TC::tile(tcs, reinterpret_cast<unsigned char *>(sBuf), tmem, tphase, a.it, g,
+                             fr_v + base, nv);
+                    if (tid < nv) {
+                        const int gi = fr_i[base + tid], gq = gi >> 16;
+                        const int32_t s = fr_v[base + tid];
+                        const float v = sc[tid];
+                        if (!isfinite(v)) atomicOr(a.nonfinite, 1);
+                        const uint64_t key = make_key(v, slot_rank(g, s));
+                        fr_key[base + tid] = key;
+                        MqQuery &Q = st.qs[gq];
+                        atomicAdd(reinterpret_cast<unsigned long long *>(&Q.per_layer[layer]), 1ull);
+                        const float Ts = orderable_f32((uint32_t)(Q.poolT >> 32));
+                        if (!Q.poolT || v >= Ts - band_of(Ts)) {
+                            const int idx = atomicAdd(&Q.nPool, 1);
+                            pkey(gq, Q.pool_cur)[idx] = key;
+                            pslot(gq, Q.pool_cur)[idx] = s;
+                            pmeta(gq, Q.pool_cur)[idx] = hop << 1;
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
+            } else {
+                int *pq = reinterpret_cast<int *>(sBuf + EX::OFF_PQ);
+                const float *sc = reinterpret_cast<const float *>(sBuf + EX::OFF_SC);
+                for (int base = 0; base < n; base += EX::PT) {
+                    const int nv = min(EX::PT, n - base);
+                    for (int pp = 0; pp < 4; ++pp) {
+                        const int p = warp * 4 + pp;
+                        float4 *xr = sBuf + EX::OFF_X0 + p * EX::LDX0;
+                        if (p < nv) {
+                            const float4 *hv = reinterpret_cast<const float4 *>(
+                                a.it.emb + slot_row(g, fr_v[base + p]) * a.it.ld);
+                            for (int cc = lane; cc < DH / 4; cc += 32)
+                                xr[chunk_perm(DH / 4 + cc, 2 * DH) - DH / 4] = __ldg(hv + cc);
+                        } else {
+                            for (int cc = lane; cc < DH / 4; cc += 32) xr[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+                        }
+                        if (lane == 0) pq[p] = p < nv ? (fr_i[base + p] >> 16) : 0;
+                    }
+                    __syncthreads();
+                    EX::tile(sW, sBuf, sAcc0, nv, a.nonfinite);
+                    if (tid < nv) {
+                        const int gq = fr_i[base + tid] >> 16;
+                        const int32_t s = fr_v[base + tid];
+                        const uint64_t key = make_key(sc[tid], slot_rank(g, s));
+                        fr_key[base + tid] = key;
+                        MqQuery &Q = st.qs[gq];
+                        atomicAdd(reinterpret_cast<unsigned long long *>(&Q.per_layer[layer]), 1ull);
+                        if (key > Q.poolT) {
+                            const int idx = atomicAdd(&Q.nPool, 1);
+                            pkey(gq, Q.pool_cur)[idx] = key;
+                            pslot(gq, Q.pool_cur)[idx] = s;
+                            pmeta(gq, Q.pool_cur)[idx] = (hop << 1) | 1;
+                        }
+                    }
+                    __syncthreads();
+                }
+            }
+        };
+        // exact re-score of rq[0..n): entry = (gq << 24 | idx) with idx into that query's
+        // current pool (pool=1) or into the seg arrays (pool=0, gq from the seg entry)
+        auto rescore = [&](int n, bool pool) {
+            if constexpr (MODE == 1) {
+                int *pq = reinterpret_cast<int *>(sBuf + EX::OFF_PQ);
+                const float *sc = reinterpret_cast<const float *>(sBuf + EX::OFF_SC);
+                for (int base = 0; base < n; base += EX::PT) {
+                    const int nv = min(EX::PT, n - base);
+                    for (int pp = 0; pp < 4; ++pp) {
+                        const int p = warp * 4 + pp;
+                        float4 *xr = sBuf + EX::OFF_X0 + p * EX::LDX0;
+                        if (p < nv) {
+                            const int e = rq[base + p];
+                            const int gq = e >> 24, idx = e & 0xFFFFFF;
+                            const int32_t s = pool ? pslot(gq, st.qs[gq].pool_cur)[idx] : seg_v[idx];
+                            const float4 *hv = reinterpret_cast<const float4 *>(a.it.emb + slot_row(g, s) * a.it.ld);
+                            for (int cc = lane; cc < DH / 4; cc += 32)
+                                xr[chunk_perm(DH / 4 + cc, 2 * DH) - DH / 4] = __ldg(hv + cc);
+                            if (lane == 0) pq[p] = gq;
+                        } else {
+                            for (int cc = lane; cc < DH / 4; cc += 32) xr[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
+                            if (lane == 0) pq[p] = 0;
+                        }
+                    }
+                    __syncthreads();
+                    EX::tile(sW, sBuf, sAcc0, nv, a.nonfinite);
+                    if (tid < nv) {
+                        const int e = rq[base + tid];
+                        const int gq = e >> 24, idx = e & 0xFFFFFF;
+                        if (pool) {
+                            const int c = st.qs[gq].pool_cur;
+                            pkey(gq, c)[idx] = make_key(sc[tid], slot_rank(g, pslot(gq, c)[idx]));
+                            pmeta(gq, c)[idx] |= 1;
+                        } else {
+                            seg_key[idx] = make_key(sc[tid], slot_rank(g, seg_v[idx]));
+                            seg_ex[idx] = 1;
+                        }
+                    }
+                    __syncthreads();
+                }
+                if (tid == 0 && n) atomicAdd(a.counters, (unsigned long long)n);
+            }
+        };
+        // collect non-exact pool entries of every query with pred(gq, score) into rq
+        auto collect_pool = [&](auto pred) {
+            if (tid == 0) st.nRq = 0;
+            __syncthreads();
+            for (int gq = 0; gq < G; ++gq) {
+                const MqQuery &Q = st.qs[gq];
+                const int np = Q.nPool;
+                const uint64_t *pk = pkey(gq, Q.pool_cur);
+                const int32_t *pm = pmeta(gq, Q.pool_cur);
+                for (int i0 = 0; i0 < np; i0 += NT) {
+                    const int i = i0 + tid;
+                    bool ok = i < np && !(pm[i] & 1) && pred(gq, orderable_f32((uint32_t)(pk[i] >> 32)));
+                    warp_append2(ok, (gq << 24) | i, 0, &st.nRq, rq, surv_i);
+                }
+            }
+            __syncthreads();
+            return st.nRq;
+        };
+        // per-query pool compaction to top-k (warp gq), tensor mode refines the band first
+        auto compact_pools = [&]() {
+            if constexpr (MODE == 1) {
+                __shared__ float thr[mq::G];
+                if (warp < G) {
+                    const MqQuery &Q = st.qs[warp];
+                    float Ts = INFINITY;
+                    if (Q.nPool > a.k) {
+                        const uint64_t Ta = warp_select_threshold(pkey(warp, Q.pool_cur), Q.nPool, a.k, hist + warp * 256);
+                        Ts = orderable_f32((uint32_t)(Ta >> 32));
+                    }
+                    if (lane == 0) thr[warp] = Ts;
+                }
+                __syncthreads();
+                const int n = collect_pool([&](int gq, float v) {
+                    return isfinite(thr[gq]) && fabsf(v - thr[gq]) <= band_of(thr[gq]);
+                });
+                rescore(n, true);
+            }
+            if (warp < G) {
+                MqQuery &Q = st.qs[warp];
+                if (Q.nPool > a.k) {
+                    const int c = Q.pool_cur, np = Q.nPool;
+                    const uint64_t T = warp_select_threshold(pkey(warp, c), np, a.k, hist + warp * 256);
+                    int cnt = 0;
+                    for (int i0 = 0; i0 < np; i0 += 32) {
+                        const int i = i0 + lane;
+                        const bool keep = i < np && pkey(warp, c)[i] >= T;
+                        const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                        if (keep) {
+                            const int pos = cnt + __popc(mask & ((1u << lane) - 1u));
+                            pkey(warp, c ^ 1)[pos] = pkey(warp, c)[i];
+                            pslot(warp, c ^ 1)[pos] = pslot(warp, c)[i];
+                            pmeta(warp, c ^ 1)[pos] = pmeta(warp, c)[i];
+                        }
+                        cnt += __popc(mask);
+                    }
+                    __syncwarp();
+                    if (lane == 0) { Q.pool_cur = c ^ 1; Q.nPool = cnt; Q.poolT = T; }
+                }
+            }
+            __syncthreads();
+        };
+        // owner resolution: survivors whose tag still carries their code own the node
+        auto resolve = [&](int nS) {
+            for (int t0 = 0; t0 < nS; t0 += NT) {
+                const int t = t0 + tid;
+                bool ok = false;
+                int32_t v = 0, gi = 0;
+                if (t < nS) {
+                    v = surv_v[t];
+                    gi = surv_i[t];
+                    const int gq = gi >> 16;
+                    if (__ldcg(reinterpret_cast<const unsigned long long *>(tags_of(gq) + v)) ==
+                        claim_code(st.qs[gq].epoch, gi & 0xFFFF))
+                        ok = true;
+                }
+                warp_append2(ok, v, gi, &st.nFresh, fr_v, fr_i);
+            }
+            __syncthreads();
+            const int nF = st.nFresh;
+            for (int t = tid; t < nF; t += NT) {
+                const int gq = fr_i[t] >> 16;
+                tags_of(gq)[fr_v[t]] = done_code(st.qs[gq].epoch);
+            }
+            __syncthreads();
+        };
+        // sort each query's pool (group of GT threads per query, named barrier 1 + gq)
+        auto sort_pools = [&]() {
+            const int gq = tid / mq::GT, gt = tid % mq::GT;
+            const MqQuery &Q = st.qs[gq];
+            uint64_t *sk = sortk + gq * a.sortcap;
+            int32_t *sv = sortv + gq * a.sortcap;
+            const int np = Q.nPool;
+            for (int i = gt; i < np; i += mq::GT) { sk[i] = pkey(gq, Q.pool_cur)[i]; sv[i] = i; }
+            group_sort_desc<mq::GT>(sk, sv, np, a.sortcap, gt, 1 + gq);
+            __syncthreads();
+        };
+
+        // ================= init: entry + its top-layer neighbourhood (hop 0)
+        if (tid == 0) { st.nS = 0; st.nFresh = 0; }
+        __syncthreads();
+        if (tid < G && st.qs[tid].q >= 0) {
+            const int idx = atomicAdd(&st.nFresh, 1);
+            tags_of(tid)[g.entry] = done_code(st.qs[tid].epoch);
+            fr_v[idx] = g.entry;
+            fr_i[idx] = tid << 16;
+        }
+        if (warp < G && st.qs[warp].q >= 0) {
+            const int32_t *row = graph_row(g, top, g.entry);
+            uint64_t *tg = tags_of(warp);
+            if (lane == 0) st.qs[warp].rows += 1;
+            if (row) {
+                const uint64_t code = claim_code(st.qs[warp].epoch, 0);
+                for (int c0 = 0; c0 < g.deg[top]; c0 += 32) {
+                    const int32_t v = (c0 + lane < g.deg[top]) ? __ldg(row + c0 + lane) : -1;
+                    const unsigned nv = __popc(__ballot_sync(0xffffffffu, v >= 0));
+                    if (lane == 0) st.qs[warp].nbrs += nv;
+                    bool ok = false;
+                    if (v >= 0) {
+                        const uint64_t old = atomicMax(reinterpret_cast<unsigned long long *>(tg + v), code);
+                        ok = old < code;
+                    }
+                    warp_append2(ok, v, warp << 16, &st.nS, surv_v, surv_i);
+                }
+            }
+        }
+        __syncthreads();
+        resolve(st.nS);
+        score_fresh(st.nFresh, top, 0);
+        compact_pools();
+
+        int h = 0;
+        for (int layer = top; layer >= 0; --layer) {
+            // ---- seeds: each query's pool sorted, first min(kp, |pool|) (exact in MODE 1)
+            if constexpr (MODE == 1) {
+                __shared__ float thr2[mq::G];
+                if (warp < G) {
+                    const MqQuery &Q = st.qs[warp];
+                    float Ts = -INFINITY;  // all entries when |pool| <= kp
+                    if (Q.nPool > a.kp) {
+                        const uint64_t Ta = warp_select_threshold(pkey(warp, Q.pool_cur), Q.nPool, a.kp, hist + warp * 256);
+                        Ts = orderable_f32((uint32_t)(Ta >> 32));
+                        Ts = Ts - band_of(Ts);
+                    }
+                    if (lane == 0) thr2[warp] = Ts;
+                }
+                __syncthreads();
+                rescore(collect_pool([&](int gq, float v) { return v >= thr2[gq]; }), true);
+            }
+            sort_pools();
+            if (tid == 0) {
+                int off = 0;
+                for (int gq = 0; gq < G; ++gq) {
+                    MqQuery &Q = st.qs[gq];
+                    const int ns = Q.q >= 0 ? min(a.kp, Q.nPool) : 0;
+                    Q.f_off = off;
+                    Q.f_cnt = ns;
+                    off += ns;
+                }
+                st.nF = off;
+                st.f_cur = 0;
+            }
+            __syncthreads();
+            for (int gq = 0; gq < G; ++gq) {
+                const MqQuery &Q = st.qs[gq];
+                for (int i = tid; i < Q.f_cnt; i += NT) {
+                    fslot[0][Q.f_off + i] = pslot(gq, Q.pool_cur)[sortv[gq * a.sortcap + i]];
+                    fsrch[0][Q.f_off + i] = (gq << 16) | i;
+                }
+            }
+            __syncthreads();
+            const int deg = g.deg[layer];
+            for (int t = 0; t < a.hops; ++t) {
+                ++h;
+                const int nF = st.nF;
+                if (nF == 0) { h += a.hops - 1 - t; break; }
+                const int fc = st.f_cur;
+                if (tid == 0) { st.nS = 0; st.nFresh = 0; }
+                __syncthreads();
+                // ---- expand + claim, 4 frontier rows in flight per warp
+                for (int e0 = warp * 4; e0 < nF; e0 += NW * 4) {
+                    int32_t s[4], gi[4];
+                    const int32_t *row[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const int e = e0 + u;
+                        s[u] = e < nF ? fslot[fc][e] : -1;
+                        gi[u] = e < nF ? fsrch[fc][e] : 0;
+                        row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
+                    }
+                    int nvalid[4] = {0, 0, 0, 0};
+                    for (int c0 = 0; c0 < deg; c0 += 32) {
+                        int32_t v[4];
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            v[u] = (row[u] && c0 + lane < deg) ? __ldg(row[u] + c0 + lane) : -1;
+                            nvalid[u] += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
+                        }
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            bool ok = false;
+                            if (v[u] >= 0) {
+                                const int gq = gi[u] >> 16;
+                                const uint64_t code = claim_code(st.qs[gq].epoch, gi[u] & 0xFFFF);
+                                const uint64_t old = atomicMax(
+                                    reinterpret_cast<unsigned long long *>(tags_of(gq) + v[u]), code);
+                                ok = old < code;
+                            }
+                            warp_append2(ok, v[u], gi[u], &st.nS, surv_v, surv_i);
+                        }
+                    }
+                    if (lane == 0) {
+#pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (s[u] >= 0) {
+                                MqQuery &Q = st.qs[gi[u] >> 16];
+                                atomicAdd(reinterpret_cast<unsigned long long *>(&Q.rows), 1ull);
+                                atomicAdd(reinterpret_cast<unsigned long long *>(&Q.nbrs), (unsigned long long)nvalid[u]);
+                            }
+                    }
+                }
+                __syncthreads();
+                resolve(st.nS);
+                const int nFresh = st.nFresh;
+                score_fresh(nFresh, layer, h);
+                compact_pools();
+                if (t == a.hops - 1) break;
+                // ---- per-(query, searcher) top-ef of fresh claims -> next frontier
+                for (int i = tid; i < NSEG; i += NT) seg_cnt[i] = 0;
+                __syncthreads();
+                auto seg_of = [&](int gi) { return (gi >> 16) * a.kp + (gi & 0xFFFF); };
+                for (int t2 = tid; t2 < nFresh; t2 += NT) atomicAdd(&seg_cnt[seg_of(fr_i[t2])], 1);
+                __syncthreads();
+                if (warp == 0) { // exclusive scans of counts and min(count, ef)
+                    int acc = 0, accf = 0;
+                    for (int i0 = 0; i0 < NSEG; i0 += 32) {
+                        const int i = i0 + lane;
+                        const int c = i < NSEG ? seg_cnt[i] : 0, cf = min(c, a.ef);
+                        int x = c, xf = cf;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(0xffffffffu, x, o), yf = __shfl_up_sync(0xffffffffu, xf, o);
+                            if (lane >= o) { x += y; xf += yf; }
+                        }
+                        if (i < NSEG) { seg_off[i] = acc + x - c; fn_off[i] = accf + xf - cf; seg_cnt[i] = 0; }
+                        acc += __shfl_sync(0xffffffffu, x, 31);
+                        accf += __shfl_sync(0xffffffffu, xf, 31);
+                    }
+                    if (lane == 0) st.nFn = accf;
+                }
+                __syncthreads();
+                for (int t2 = tid; t2 < nFresh; t2 += NT) {
+                    const int sg = seg_of(fr_i[t2]);
+                    const int pos = seg_off[sg] + atomicAdd(&seg_cnt[sg], 1);
+                    seg_v[pos] = fr_v[t2];
+                    seg_key[pos] = fr_key[t2];
+                }
+                __syncthreads();
+                if constexpr (MODE == 1) {
+                    for (int t2 = tid; t2 < nFresh; t2 += NT) seg_ex[t2] = 0;
+                    if (tid == 0) st.nRq = 0;
+                    __syncthreads();
+                    for (int sg = warp; sg < NSEG; sg += NW) {
+                        const int ni = seg_cnt[sg], off = seg_off[sg], gq = sg / a.kp;
+                        if (ni <= a.ef) continue;
+                        const uint64_t Ta = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
+                        const float Ts = orderable_f32((uint32_t)(Ta >> 32)), bd = band_of(Ts);
+                        for (int j0 = 0; j0 < ni; j0 += 32) {
+                            const int j = j0 + lane;
+                            const bool in = j < ni &&
+                                fabsf(orderable_f32((uint32_t)(seg_key[off + j] >> 32)) - Ts) <= bd;
+                            warp_append2(in, (gq << 24) | (off + j), 0, &st.nRq, rq, surv_i);
+                        }
+                    }
+                    __syncthreads();
+                    rescore(st.nRq, false);
+                }
+                const int fn = fc ^ 1;
+                for (int sg = warp; sg < NSEG; sg += NW) {
+                    const int ni = seg_cnt[sg], off = seg_off[sg], fo = fn_off[sg];
+                    const int gi = ((sg / a.kp) << 16) | (sg % a.kp);
+                    if (ni <= a.ef) {
+                        for (int j = lane; j < ni; j += 32) { fslot[fn][fo + j] = seg_v[off + j]; fsrch[fn][fo + j] = gi; }
+                    } else {
+                        const uint64_t T = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
+                        int cnt = 0;
+                        for (int j0 = 0; j0 < ni; j0 += 32) {
+                            const int j = j0 + lane;
+                            const bool keep = j < ni && seg_key[off + j] >= T;
+                            const unsigned mask = __ballot_sync(0xffffffffu, keep);
+                            if (keep) {
+                                const int pos = fo + cnt + __popc(mask & ((1u << lane) - 1u));
+                                fslot[fn][pos] = seg_v[off + j];
+                                fsrch[fn][pos] = gi;
+                            }
+                            cnt += __popc(mask);
+                        }
+                    }
+                }
+                __syncthreads();
+                if (tid == 0) { st.nF = st.nFn; st.f_cur = fn; }
+                __syncthreads();
+            }
+        }
+
+        // ---- results: every query's pool sorted, first min(k, |pool|), exact scores
+        if constexpr (MODE == 1) rescore(collect_pool([&](int, float) { return true; }), true);
+        sort_pools();
+        for (int gq = 0; gq < G; ++gq) {
+            MqQuery &Q = st.qs[gq];
+            if (Q.q < 0) continue;
+            const int64_t q = Q.q;
+            const int np = Q.nPool, c = Q.pool_cur, nr = min(a.k, np);
+            const int32_t *sv = sortv + gq * a.sortcap;
+            for (int j = tid; j < a.k; j += NT) {
+                if (j < nr) {
+                    const int idx = sv[j];
+                    a.out_ids[q * a.k + j] = g.ids[pslot(gq, c)[idx]];
+                    a.out_scores[q * a.k + j] = (double)orderable_f32((uint32_t)(pkey(gq, c)[idx] >> 32));
+                } else {
+                    a.out_ids[q * a.k + j] = -1;
+                    a.out_scores[q * a.k + j] = __longlong_as_double(0x7ff8000000000000ll);
+                }
+            }
+            if (tid == 0) {
+                a.out_count[q] = nr;
+                int64_t ev = 0;
+                for (int l = 0; l < g.n_layers; ++l) { ev += Q.per_layer[l]; a.out_stats[q * nst + 5 + l] = Q.per_layer[l]; }
+                a.out_stats[q * nst + 0] = ev;
+                a.out_stats[q * nst + 1] = ev;
+                a.out_stats[q * nst + 2] = nr > 0 ? (pmeta(gq, c)[sv[0]] >> 1) : -1;
+                a.out_stats[q * nst + 3] = Q.rows;
+                a.out_stats[q * nst + 4] = Q.nbrs;
+            }
+        }
+    }
+    if constexpr (MODE == 1) {
+        tc::fence_before();
+        __syncthreads();
+        if (warp == 0)
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+    }
+}

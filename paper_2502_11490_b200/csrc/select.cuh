@@ -68,6 +68,7 @@ __device__ uint64_t warp_select_threshold(const uint64_t *keys, int n, int m, ui
 
 // CTA-cooperative version (all GR_NT threads call it).  hist: 256 shared u32;
 // bcast: 4 shared u32 scratch.
+template <int NT = GR_NT>
 __device__ uint64_t cta_select_threshold(const uint64_t *keys, int n, int m, uint32_t *hist,
                                          uint32_t *bcast) {
     const int tid = threadIdx.x;
@@ -75,9 +76,9 @@ __device__ uint64_t cta_select_threshold(const uint64_t *keys, int n, int m, uin
     uint32_t rem = (uint32_t)m;
     for (int shift = 56; shift >= 0; shift -= 8) {
         const uint64_t hm = high_mask(shift);
-        for (int b = tid; b < 256; b += GR_NT) hist[b] = 0;
+        for (int b = tid; b < 256; b += NT) hist[b] = 0;
         __syncthreads();
-        for (int i = tid; i < n; i += GR_NT) {
+        for (int i = tid; i < n; i += NT) {
             const uint64_t k = keys[i];
             if (((k ^ prefix) & hm) == 0) atomicAdd(&hist[(k >> shift) & 255], 1u);
         }
@@ -99,12 +100,13 @@ __device__ uint64_t cta_select_threshold(const uint64_t *keys, int n, int m, uin
 
 // CTA bitonic sort, descending by key, of n entries (keys, vals) in shared memory
 // padded to cap (power of two >= n).  Padding keys are 0 (below every real key).
+template <int NT = GR_NT>
 __device__ void cta_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap) {
-    for (int i = n + threadIdx.x; i < cap; i += GR_NT) { keys[i] = 0ull; vals[i] = -1; }
+    for (int i = n + threadIdx.x; i < cap; i += NT) { keys[i] = 0ull; vals[i] = -1; }
     __syncthreads();
     for (int size = 2; size <= cap; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < cap; i += GR_NT) {
+            for (int i = threadIdx.x; i < cap; i += NT) {
                 const int j = i ^ stride;
                 if (j > i) {
                     const bool desc = (i & size) == 0;
@@ -116,6 +118,30 @@ __device__ void cta_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap) {
                 }
             }
             __syncthreads();
+        }
+    }
+}
+
+// Bitonic sort (descending) by a group of GT threads synchronised with named barrier `bar`
+// (bar >= 1; barrier 0 is __syncthreads).  gtid: thread index inside the group.
+template <int GT>
+__device__ void group_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap, int gtid, int bar) {
+    for (int i = n + gtid; i < cap; i += GT) { keys[i] = 0ull; vals[i] = -1; }
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(GT) : "memory");
+    for (int size = 2; size <= cap; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int i = gtid; i < cap; i += GT) {
+                const int j = i ^ stride;
+                if (j > i) {
+                    const bool desc = (i & size) == 0;
+                    const uint64_t a = keys[i], b = keys[j];
+                    if (desc ? (a < b) : (a > b)) {
+                        keys[i] = b; keys[j] = a;
+                        const int32_t t = vals[i]; vals[i] = vals[j]; vals[j] = t;
+                    }
+                }
+            }
+            asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(GT) : "memory");
         }
     }
 }
