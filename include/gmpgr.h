@@ -105,6 +105,12 @@ int gr_score_pairs(const gr_model *m, const gr_items *it, const float *users, in
                    const int32_t *user_index, const int64_t *item_ids, int64_t n,
                    double *out_scores, int on_device, void *stream);
 
+/* First-pass tensor-core (split-bf16 tcgen05) scores of one user (host fp32 [d_h]) against
+ * item rows (host int64 [n]) -> host fp64 [n].  Diagnostic for the tc mode's refinement band:
+ * compare with gr_score_pairs.  GR_EINVAL if the model has no tensor-core shape. */
+int gr_score_items_approx(const gr_model *m, const gr_items *it, const float *user,
+                          const int64_t *item_ids, int64_t n, double *out_scores);
+
 /* Scratch owner for gr_search (visited tags, frontiers, pools).  One per stream. */
 int gr_searcher_create(int device, gr_searcher **out);
 int gr_searcher_destroy(gr_searcher *s);

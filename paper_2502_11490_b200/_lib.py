@@ -15,7 +15,7 @@ import numpy as np
 from .errors import DeviceError, InvalidArgumentError, NumericError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgmpgr.so")
+LIB_PATH = os.environ.get("GMPGR_LIB") or os.path.join(HERE, "libgmpgr.so")
 
 GR_OK, GR_EINVAL, GR_ENUMERIC, GR_ECUDA, GR_ENOMEM = 0, 1, 2, 3, 4
 
@@ -25,7 +25,7 @@ EXPORTS = (
     "gr_model_create", "gr_model_destroy",
     "gr_graph_create", "gr_graph_destroy",
     "gr_items_create", "gr_items_destroy",
-    "gr_score_pairs",
+    "gr_score_pairs", "gr_score_items_approx",
     "gr_searcher_create", "gr_searcher_destroy",
     "gr_search", "gr_search_async", "gr_searcher_status", "gr_searcher_launches",
     "gr_searcher_counters",
@@ -60,6 +60,7 @@ def _declare(lib):
         "gr_items_create": (C.c_int, [C.c_int, vp, i64, i32, C.c_int, vp]),
         "gr_items_destroy": (C.c_int, [vp]),
         "gr_score_pairs": (C.c_int, [vp, vp, vp, i64, vp, vp, i64, vp, C.c_int, vp]),
+        "gr_score_items_approx": (C.c_int, [vp, vp, vp, vp, i64, vp]),
         "gr_searcher_create": (C.c_int, [C.c_int, vp]),
         "gr_searcher_destroy": (C.c_int, [vp]),
         "gr_search": (C.c_int, [vp, vp, vp, vp, vp, i64, vp, vp, vp, vp, vp, C.c_int, vp]),

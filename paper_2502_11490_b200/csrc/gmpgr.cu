@@ -122,7 +122,7 @@ struct gr_items {
 struct gr_searcher {
     int device;
     int64_t slots = 0, n = 0, capF = 0, capS = 0, capP = 0;
-    uint64_t *tags = nullptr;
+    uint32_t *tags = nullptr;
     uint32_t *epochs = nullptr;
     int32_t *f_slot = nullptr, *f_srch = nullptr, *surv_v = nullptr, *surv_i = nullptr,
             *fr_v = nullptr, *fr_i = nullptr, *seg_v = nullptr, *pool_slot = nullptr;
@@ -604,7 +604,7 @@ int ensure_search_scratch(gr_searcher *S, const gr_graph *G, int64_t slots, int6
     if ((rc = dmalloc(&S->pool_key, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&S->pool_slot, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&S->pool_meta, (size_t)slots * 2 * capP))) return rc;
-    GR_CUDA(cudaMemset(S->tags, 0, (size_t)slots * n * 8));
+    GR_CUDA(cudaMemset(S->tags, 0, (size_t)slots * n * 4));
     GR_CUDA(cudaMemset(S->epochs, 0, (size_t)slots * 4));
     S->slots = slots;
     S->n = n;
@@ -622,6 +622,7 @@ int check_params(const gr_search_params *p) {
     if (p->ef < 1) return fail(GR_EINVAL, "ef must be >= 1");
     if (p->k > 8192) return fail(GR_EINVAL, "k > 8192 not supported on the device path");
     if (p->mode != GR_MODE_EXACT && p->mode != GR_MODE_TC) return fail(GR_EINVAL, "unknown mode");
+    if (p->k_parallel > 4094) return fail(GR_EINVAL, "k_parallel > 4094 not supported (claim tag width)");
     return GR_OK;
 }
 
@@ -631,7 +632,7 @@ int plan_mq(int k, int kp, SearchArgs &a) {
     using TC = TcQ<DH, ZZ>;
     SmemPlan P;
     a.off_w0 = P.alloc(EX::W_END * 16);
-    a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, TC::A_BYTES));
+    a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
     a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
     a.off_acc0 = P.alloc(mq::G * 64 * 16);
     a.off_hist = P.alloc(mq::NW * 256 * 4);
@@ -716,6 +717,58 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     GR_CUDA(cudaGetLastError());
     S->launches += 1;
     return GR_OK;
+}
+
+// approximate (first-pass) tensor-core scores of one user against item rows: error studies
+template <int DH, int ZZ>
+__global__ void __launch_bounds__(GR_NT, 1) tc_pairs_kernel(DevModel M, DevItems it, const float *user,
+                                                            const int32_t *rows, int64_t n, double *out) {
+    using T = TcMlp<DH, ZZ>;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int tid = threadIdx.x, warp = tid >> 5;
+    const uint4 *src = reinterpret_cast<const uint4 *>(M.tcB);
+    uint4 *dst = reinterpret_cast<uint4 *>(smem + T::OFF_B0H);
+    for (int t = tid; t < (T::OFF_AH - T::OFF_B0H) / 16; t += GR_NT) dst[t] = src[t];
+    float *b1 = reinterpret_cast<float *>(smem + T::OFF_B1);
+    for (int t = tid; t < 64; t += GR_NT) b1[t] = M.tcMisc[t];
+    float *w2 = reinterpret_cast<float *>(smem + T::OFF_W2);
+    for (int t = tid; t < 64 * ZZ; t += GR_NT) w2[t] = M.tcMisc[64 + t];
+    if (tid < 4) {
+        reinterpret_cast<float *>(smem + T::OFF_B2)[tid] = M.tcMisc[64 + 64 * ZZ + tid];
+        reinterpret_cast<float *>(smem + T::OFF_ATT)[tid] = M.tcMisc[68 + 64 * ZZ + tid];
+    }
+    for (int o = tid; o < 64; o += GR_NT) {
+        float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int j = 0; j < M.pre_ch; ++j) {
+            const int c = chunk_perm(j, 2 * DH);
+            mac4(acc, make_float4(user[4 * c], user[4 * c + 1], user[4 * c + 2], user[4 * c + 3]),
+                 M.W[0][j * 64 + o]);
+        }
+        reinterpret_cast<float *>(smem + T::OFF_U)[o] = __fadd_rn(hsum4(acc), M.b[0][o]);
+    }
+    uint32_t *tptr = reinterpret_cast<uint32_t *>(smem + T::OFF_TMEM);
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         tc::smem_u32(tptr)), "r"(128));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    if (tid == 0) tc::mbar_init(reinterpret_cast<uint64_t *>(smem + T::OFF_BAR), 1);
+    tc::fence_before();
+    __syncthreads();
+    tc::fence_after();
+    const uint32_t tmem = *tptr;
+    uint32_t phase = 0;
+    DevGraph g;
+    memset(&g, 0, sizeof(g));
+    for (int64_t base = (int64_t)blockIdx.x * T::TM; base < n; base += (int64_t)gridDim.x * T::TM) {
+        const int nv = (int)min((int64_t)T::TM, n - base);
+        T::tile(smem, tmem, phase, it, g, rows + base, nv);
+        if (tid < nv) out[base + tid] = (double)reinterpret_cast<const float *>(smem + T::OFF_SC)[tid];
+        __syncthreads();
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
 }
 
 int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I,
@@ -1002,6 +1055,48 @@ int gr_score_pairs(const gr_model *m, const gr_items *it, const float *users, in
     if (hflags[1]) return fail(GR_EINVAL, "user index or item id out of range");
     if (hflags[0]) return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
     return GR_OK;
+}
+
+// ------------------------------------------------------------------ approximate pairs
+int gr_score_items_approx(const gr_model *m, const gr_items *it, const float *user,
+                          const int64_t *item_ids, int64_t n, double *out_scores) {
+    if (!m || !it || !user || !item_ids || !out_scores) return fail(GR_EINVAL, "null argument");
+    const int shape = fixed_shape(m->dm);
+    if (!shape || !m->dm.tc_ok) return fail(GR_EINVAL, "model shape has no tensor-core scorer");
+    if (m->dm.d_h != it->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
+    if (n <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(m->device));
+    std::vector<int32_t> rows(n);
+    for (int64_t i = 0; i < n; ++i) {
+        if (item_ids[i] < 0 || item_ids[i] >= it->di.n) return fail(GR_EINVAL, "item id out of range");
+        rows[i] = (int32_t)item_ids[i];
+    }
+    float *du = nullptr;
+    int32_t *dr = nullptr;
+    double *dout = nullptr;
+    if (int rc = dmalloc(&du, (size_t)m->dm.d_h)) return rc;
+    if (int rc = dmalloc(&dr, (size_t)n)) { cudaFree(du); return rc; }
+    if (int rc = dmalloc(&dout, (size_t)n)) { cudaFree(du); cudaFree(dr); return rc; }
+    cudaMemcpy(du, user, m->dm.d_h * 4, cudaMemcpyHostToDevice);
+    cudaMemcpy(dr, rows.data(), n * 4, cudaMemcpyHostToDevice);
+    void (*kern)(DevModel, DevItems, const float *, const int32_t *, int64_t, double *) = nullptr;
+    int smem = 0;
+    switch (shape) {
+    case 1283: kern = tc_pairs_kernel<128, 3>; smem = TcMlp<128, 3>::BYTES; break;
+    case 1282: kern = tc_pairs_kernel<128, 2>; smem = TcMlp<128, 2>::BYTES; break;
+    case 643: kern = tc_pairs_kernel<64, 3>; smem = TcMlp<64, 3>::BYTES; break;
+    default: kern = tc_pairs_kernel<64, 2>; smem = TcMlp<64, 2>::BYTES; break;
+    }
+    int rc = set_smem(kern, smem);
+    if (rc == GR_OK) {
+        const int grid = (int)std::min<int64_t>((n + 127) / 128, num_sms(m->device));
+        kern<<<grid, GR_NT, smem>>>(m->dm, it->di, du, dr, n, dout);
+        cudaError_t e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) rc = fail(GR_ECUDA, cudaGetErrorString(e));
+        else cudaMemcpy(out_scores, dout, n * 8, cudaMemcpyDeviceToHost);
+    }
+    cudaFree(du); cudaFree(dr); cudaFree(dout);
+    return rc;
 }
 
 // ------------------------------------------------------------------ brute force

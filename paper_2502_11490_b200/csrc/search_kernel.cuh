@@ -35,7 +35,7 @@ struct SearchArgs {
     int32_t *out_count;
     int64_t *out_stats;
     // per-slot scratch
-    uint64_t *tags;    // [slots][n]
+    uint32_t *tags;    // [slots][n] epoch-stamped claim tags
     uint32_t *epochs;  // [slots]
     int32_t *f_slot;   // [slots][2][capF]
     int32_t *f_srch;   // [slots][2][capF]
@@ -64,6 +64,7 @@ struct SearchArgs {
 struct CtaState {
     int q;
     uint32_t epoch;
+    int wrap;
     int nF, nS, nFresh, nPool, nPool2, nFn;
     int pool_cur, f_cur;
     uint64_t poolT, hopmax, best;
@@ -73,11 +74,21 @@ struct CtaState {
     uint32_t bcast[4];
 };
 
-__device__ __forceinline__ uint64_t claim_code(uint32_t epoch, int i) {
-    return ((uint64_t)epoch << 32) | (uint64_t)(0xFFFFFFFEu - (uint32_t)i);
+// u32 tag = epoch (20 bits) << 12 | code: claim code 0xFFE - searcher (atomicMax keeps the
+// lowest searcher), 0xFFF = owned.  A tag below epoch << 12 is "unclaimed in this query".
+// Epochs wrap every 2^20 - 1 queries per slot: the slot's array is then cleared (tag_epoch).
+#define GR_EPOCH_MAX ((1u << 20) - 1u)
+__device__ __forceinline__ uint32_t claim_code(uint32_t epoch, int i) {
+    return (epoch << 12) | (0xFFEu - (uint32_t)i);
 }
-__device__ __forceinline__ uint64_t done_code(uint32_t epoch) {
-    return ((uint64_t)epoch << 32) | 0xFFFFFFFFull;
+__device__ __forceinline__ uint32_t done_code(uint32_t epoch) { return (epoch << 12) | 0xFFFu; }
+// next epoch of a slot; on wrap the whole CTA clears that slot's tag array (rare)
+__device__ __forceinline__ uint32_t next_epoch(uint32_t *epochs, int64_t slot, uint32_t *tags,
+                                               int64_t n, int *wrap_flag) {
+    uint32_t e = epochs[slot] + 1u;
+    if (e > GR_EPOCH_MAX) { e = 1u; *wrap_flag = 1; }
+    epochs[slot] = e;
+    return e;
 }
 
 // warp-aggregated append of (v, i) when ok; returns nothing
@@ -200,7 +211,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
 
     // ---- per-slot scratch
     const int64_t slot = blockIdx.x;
-    uint64_t *tags = a.tags + slot * g.n;
+    uint32_t *tags = a.tags + slot * g.n;
     int32_t *fslot[2] = {a.f_slot + slot * 2 * a.capF, a.f_slot + slot * 2 * a.capF + a.capF};
     int32_t *fsrch[2] = {a.f_srch + slot * 2 * a.capF, a.f_srch + slot * 2 * a.capF + a.capF};
     int32_t *surv_v = a.surv_v + slot * a.capS, *surv_i = a.surv_i + slot * a.capS;
@@ -227,11 +238,8 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         __syncthreads();
         if (tid == 0) {
             st.q = atomicAdd(a.queue, 1);
-            if (st.q < a.Q) {
-                const uint32_t e = a.epochs[slot] + 1u;
-                a.epochs[slot] = e;
-                st.epoch = e;
-            }
+            st.wrap = 0;
+            if (st.q < a.Q) st.epoch = next_epoch(a.epochs, slot, tags, g.n, &st.wrap);
             st.nPool = 0; st.pool_cur = 0; st.f_cur = 0; st.poolT = 0ull;
             st.hopmax = 0ull; st.best = 0ull; st.besthop = -1;
             for (int l = 0; l < GR_MAX_LAYERS; ++l) st.per_layer[l] = 0;
@@ -240,6 +248,11 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         __syncthreads();
         const int64_t q = st.q;
         if (q >= a.Q) break;
+        if (st.wrap) {  // epoch wrapped: clear this slot's tags
+            for (int64_t i = tid; i < g.n; i += GR_NT) tags[i] = 0u;
+            __threadfence_block();
+            __syncthreads();
+        }
         if (tid == 0) ph_t0 = clock64();
         const uint32_t epoch = st.epoch;
         const float *hu = a.users + q * d_h;
@@ -436,7 +449,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
 
         // ---- owner resolution: survivors whose tag still carries their code own the node
         auto resolve = [&](int nS, int fresh_base) {
-            const uint64_t done = done_code(epoch);
+            const uint32_t done = done_code(epoch);
             for (int t0 = 0; t0 < nS; t0 += GR_NT) {
                 const int t = t0 + tid;
                 bool ok = false;
@@ -445,8 +458,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     v = surv_v[t];
                     i = surv_i[t];
                     // L2 read: the tag was last written by atomics (performed at L2)
-                    if (__ldcg(reinterpret_cast<const unsigned long long *>(tags + v)) ==
-                        claim_code(epoch, i))
+                    if (__ldcg(tags + v) == claim_code(epoch, i))
                         ok = true;
                 }
                 __syncwarp();
@@ -473,14 +485,14 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
             const int32_t *row = graph_row(g, top, g.entry);
             if (lane == 0) st.rows += 1;
             if (row) {
-                const uint64_t code = claim_code(epoch, 0);
+                const uint32_t code = claim_code(epoch, 0);
                 for (int c0 = 0; c0 < g.deg[top]; c0 += 32) {
                     const int32_t v = (c0 + lane < g.deg[top]) ? __ldg(row + c0 + lane) : -1;
                     const unsigned nv = __popc(__ballot_sync(0xffffffffu, v >= 0));
                     if (lane == 0) st.nbrs += nv;
                     bool ok = false;
                     if (v >= 0) {
-                        const uint64_t old = atomicMax(reinterpret_cast<unsigned long long *>(tags + v), code);
+                        const uint32_t old = atomicMax(tags + v, code);
                         ok = old < code;
                     }
                     warp_append2(ok, v, 0, &st.nS, surv_v, surv_i);
@@ -554,9 +566,8 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                         for (int u = 0; u < 4; ++u) {
                             bool ok = false;
                             if (v[u] >= 0) {
-                                const uint64_t code = claim_code(epoch, srch[u]);
-                                const uint64_t old =
-                                    atomicMax(reinterpret_cast<unsigned long long *>(tags + v[u]), code);
+                                const uint32_t code = claim_code(epoch, srch[u]);
+                                const uint32_t old = atomicMax(tags + v[u], code);
                                 ok = old < code;
                             }
                             warp_append2(ok, v[u], srch[u], &st.nS, surv_v, surv_i);

@@ -17,7 +17,10 @@
 #include "tc_scorer.cuh"
 
 namespace mq {
-constexpr int NT = 512, NW = NT / 32, G = 4, GT = NT / G; // group threads for per-query sorts
+#ifndef GR_MQ_G
+#define GR_MQ_G 4
+#endif
+constexpr int NT = 512, NW = NT / 32, G = GR_MQ_G, GT = NT / G; // group threads for per-query sorts
 constexpr int PT = 4 * NW;                                   // exact tile: 64 pairs
 }  // namespace mq
 
@@ -134,7 +137,9 @@ struct ExactQ {
 // tcgen05 scorer for 512-thread CTAs: 128-pair tiles, per-pair query user half.
 template <int D_H, int Z>
 struct TcQ {
-    static constexpr int H = 64, TM = 128, KC = 64, NKC0 = D_H / KC;
+    // layer 0 in ONE K chunk (A = 128 x D_H hi/lo = 64 KB at d_h 128, inside the exact
+    // activation buffers it aliases) -> two MMA round trips per tile
+    static constexpr int H = 64, TM = 128, KC = D_H, NKC0 = 1;
     static constexpr int OFF_B0H = 0;
     static constexpr int OFF_B0L = OFF_B0H + H * D_H * 2;
     static constexpr int OFF_B1H = OFF_B0L + H * D_H * 2;
@@ -176,11 +181,12 @@ struct TcQ {
         uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
         const uint32_t aH = tc::smem_u32(Ah), aL = tc::smem_u32(Al);
         for (int kc = 0; kc < NKC0; ++kc) {
-            for (int t = tid; t < TM * 16; t += mq::NT) {
-                const int r = t >> 4, c = t & 15;
+            constexpr int CPR = KC / 4; // float4 per row chunk
+            for (int t = tid; t < TM * CPR; t += mq::NT) {
+                const int r = t / CPR, c = t % CPR;
                 if (r < nv) {
                     const float4 x = __ldg(reinterpret_cast<const float4 *>(
-                                               it.emb + slot_row(g, slots[r]) * it.ld) + kc * 16 + c);
+                                               it.emb + slot_row(g, slots[r]) * it.ld) + kc * CPR + c);
                     uint2 hi, lo;
                     tc::split4(x, hi, lo);
                     const uint32_t off = tc::kmaj_off(r, 4 * c, KC);
@@ -295,7 +301,7 @@ struct MqQuery {
 
 struct MqState {
     MqQuery qs[mq::G];
-    int nF, nS, nFresh, nFn, nRq, f_cur, base;
+    int nF, nS, nFresh, nFn, nRq, f_cur, base, wrap[mq::G];
     uint32_t bcast[4];
 };
 
@@ -306,9 +312,20 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
     using EX = ExactQ<DH, ZZ>;
     using TC = TcQ<DH, ZZ>;
     constexpr int G = mq::G, NT = mq::NT, NW = mq::NW;
-    extern __shared__ __align__(1024) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem[];
     __shared__ MqState st;
+    __shared__ unsigned long long ph_acc[8];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    long long ph_t0 = 0;
+    if (tid < 8) ph_acc[tid] = 0;
+#define GR_PH(i)                                                          \
+    do {                                                                  \
+        if (a.phase_cycles && tid == 0) {                                 \
+            const long long now_ = clock64();                             \
+            ph_acc[i] += (unsigned long long)(now_ - ph_t0);              \
+            ph_t0 = now_;                                                 \
+        }                                                                 \
+    } while (0)
     const DevModel &M = a.M;
     const DevGraph &g = a.g;
     // ---- shared memory carve (offsets from the host plan)
@@ -387,17 +404,21 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         if (tid < G) {
             MqQuery &Q = st.qs[tid];
             Q.q = st.base + tid < a.Q ? st.base + tid : -1;
-            if (Q.q >= 0) {
-                const uint32_t e = a.epochs[cta * G + tid] + 1u;
-                a.epochs[cta * G + tid] = e;
-                Q.epoch = e;
-            }
+            st.wrap[tid] = 0;
+            if (Q.q >= 0) Q.epoch = next_epoch(a.epochs, cta * G + tid, tags_of(tid), g.n, &st.wrap[tid]);
             Q.nPool = 0; Q.pool_cur = 0; Q.poolT = 0ull; Q.besthop = -1;
             for (int l = 0; l < GR_MAX_LAYERS; ++l) Q.per_layer[l] = 0;
             Q.rows = 0; Q.nbrs = 0;
         }
         if (tid == 0) { st.f_cur = 0; }
         __syncthreads();
+        for (int gq = 0; gq < G; ++gq)
+            if (st.wrap[gq]) {  // epoch wrapped: clear that slot's tags
+                uint32_t *tg = tags_of(gq);
+                for (int64_t i = tid; i < g.n; i += NT) tg[i] = 0u;
+                __syncthreads();
+            }
+        if (tid == 0) ph_t0 = clock64();
         // ---- hoisted user halves (exact acc0; tensor-core u = user half + b0)
         for (int t = tid; t < G * 64; t += NT) {
             const int gq = t >> 6, o = t & 63;
@@ -600,8 +621,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                     v = surv_v[t];
                     gi = surv_i[t];
                     const int gq = gi >> 16;
-                    if (__ldcg(reinterpret_cast<const unsigned long long *>(tags_of(gq) + v)) ==
-                        claim_code(st.qs[gq].epoch, gi & 0xFFFF))
+                    if (__ldcg(tags_of(gq) + v) == claim_code(st.qs[gq].epoch, gi & 0xFFFF))
                         ok = true;
                 }
                 warp_append2(ok, v, gi, &st.nFresh, fr_v, fr_i);
@@ -637,17 +657,17 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         }
         if (warp < G && st.qs[warp].q >= 0) {
             const int32_t *row = graph_row(g, top, g.entry);
-            uint64_t *tg = tags_of(warp);
+            uint32_t *tg = tags_of(warp);
             if (lane == 0) st.qs[warp].rows += 1;
             if (row) {
-                const uint64_t code = claim_code(st.qs[warp].epoch, 0);
+                const uint32_t code = claim_code(st.qs[warp].epoch, 0);
                 for (int c0 = 0; c0 < g.deg[top]; c0 += 32) {
                     const int32_t v = (c0 + lane < g.deg[top]) ? __ldg(row + c0 + lane) : -1;
                     const unsigned nv = __popc(__ballot_sync(0xffffffffu, v >= 0));
                     if (lane == 0) st.qs[warp].nbrs += nv;
                     bool ok = false;
                     if (v >= 0) {
-                        const uint64_t old = atomicMax(reinterpret_cast<unsigned long long *>(tg + v), code);
+                        const uint32_t old = atomicMax(tg + v, code);
                         ok = old < code;
                     }
                     warp_append2(ok, v, warp << 16, &st.nS, surv_v, surv_i);
@@ -658,6 +678,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         resolve(st.nS);
         score_fresh(st.nFresh, top, 0);
         compact_pools();
+        GR_PH(0);
 
         int h = 0;
         for (int layer = top; layer >= 0; --layer) {
@@ -699,6 +720,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                 }
             }
             __syncthreads();
+            GR_PH(1);
             const int deg = g.deg[layer];
             for (int t = 0; t < a.hops; ++t) {
                 ++h;
@@ -731,9 +753,8 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                             bool ok = false;
                             if (v[u] >= 0) {
                                 const int gq = gi[u] >> 16;
-                                const uint64_t code = claim_code(st.qs[gq].epoch, gi[u] & 0xFFFF);
-                                const uint64_t old = atomicMax(
-                                    reinterpret_cast<unsigned long long *>(tags_of(gq) + v[u]), code);
+                                const uint32_t code = claim_code(st.qs[gq].epoch, gi[u] & 0xFFFF);
+                                const uint32_t old = atomicMax(tags_of(gq) + v[u], code);
                                 ok = old < code;
                             }
                             warp_append2(ok, v[u], gi[u], &st.nS, surv_v, surv_i);
@@ -750,10 +771,14 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                     }
                 }
                 __syncthreads();
+                GR_PH(2);
                 resolve(st.nS);
+                GR_PH(3);
                 const int nFresh = st.nFresh;
                 score_fresh(nFresh, layer, h);
+                GR_PH(4);
                 compact_pools();
+                GR_PH(5);
                 if (t == a.hops - 1) break;
                 // ---- per-(query, searcher) top-ef of fresh claims -> next frontier
                 for (int i = tid; i < NSEG; i += NT) seg_cnt[i] = 0;
@@ -830,6 +855,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                 __syncthreads();
                 if (tid == 0) { st.nF = st.nFn; st.f_cur = fn; }
                 __syncthreads();
+                GR_PH(6);
             }
         }
 
@@ -863,7 +889,10 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                 a.out_stats[q * nst + 4] = Q.nbrs;
             }
         }
+        GR_PH(7);
     }
+    if (a.phase_cycles && tid < 8) atomicAdd(a.phase_cycles + tid, ph_acc[tid]);
+#undef GR_PH
     if constexpr (MODE == 1) {
         tc::fence_before();
         __syncthreads();

@@ -227,3 +227,35 @@ def test_tensor_core_mode_large_graph_equals_exact(P):
     c = s.counters()
     assert c["tensor_scored"] > 0
     assert c["exact_rescored"] < 0.5 * c["tensor_scored"], c
+
+
+def test_tc_first_pass_error_far_inside_refinement_band(P):
+    """The tc mode is exact only if |approx - exact| < band/2 (band = 1e-3*|T| + 1e-3).
+    Measure the split-bf16 tcgen05 first pass against the exact scorer on 1M pairs of the
+    BASELINE model family (d_h 128, Z 3) and require a >= 10x margin."""
+    import ctypes
+    from paper_2502_11490_b200 import _lib
+
+    rng = np.random.default_rng(21)
+    n, d = 250_000, 128
+    model = P.create_model(d_x=d, d_h=d, z_dim=3, hidden=(64, 64), seed=1)
+    centers = rng.normal(scale=4.0, size=(1024, d))
+    feats = (centers[rng.integers(0, 1024, size=n)] + rng.normal(size=(n, d))).astype(np.float32)
+    emb = np.ascontiguousarray(model.item_embeddings(feats), dtype=np.float32)
+    users = model.user_embedding(rng.normal(size=(4, d)).astype(np.float32)).astype(np.float32)
+    dm = model.metric.device_model(0)
+    it = _lib.DeviceItems(emb, 0)
+    ids = np.arange(n, dtype=np.int64)
+    worst = 0.0
+    for u in users:
+        u = np.ascontiguousarray(u)
+        approx = np.empty(n)
+        _lib.check(_lib.lib().gr_score_items_approx(dm.h, it.h, _lib.ptr(u), _lib.ptr(ids), n,
+                                                    _lib.ptr(approx)))
+        exact = np.empty(n)
+        _lib.check(_lib.lib().gr_score_pairs(dm.h, it.h, _lib.ptr(u), 1, None, _lib.ptr(ids), n,
+                                             _lib.ptr(exact), 0, None))
+        band = 1e-3 * np.abs(exact) + 1e-3
+        worst = max(worst, float(np.max(np.abs(approx - exact) / band)))
+    print(f"max |approx-exact| / band = {worst:.3e}")
+    assert worst < 0.05
