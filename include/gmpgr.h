@@ -139,7 +139,9 @@ int64_t gr_searcher_launches(const gr_searcher *s);
 /* cumulative scoring counters of this searcher: out[0] = exact re-scores (tensor-core
  * mode), out[1] = tensor-core scores; when the searcher was created with
  * GMPGR_PHASE_TIMING=1 in the environment, out[2..9] = summed SM cycles per search phase
- * (init, seeds, expand, resolve, score, pool, frontier, output).  out must hold 10 values.
+ * (init, seeds, expand, resolve, score, pool, frontier, output) and out[10..14] = cycles
+ * inside tensor-core tiles (gather, layer-0 MMA wait, epilogue 0, layer-1 MMA wait,
+ * epilogue 1).  out must hold 18 values.
  * Synchronises the device. */
 int gr_searcher_counters(gr_searcher *s, int64_t *out);
 

@@ -233,11 +233,14 @@ class DeviceSearcher(_Handle):
         return int(lib().gr_searcher_launches(self.h))
 
     def counters(self) -> dict:
-        out = np.zeros(10, dtype=np.int64)
+        out = np.zeros(18, dtype=np.int64)
         check(lib().gr_searcher_counters(self.h, ptr(out)))
         d = {"exact_rescored": int(out[0]), "tensor_scored": int(out[1])}
-        if out[2:].any():
+        if out[2:10].any():
             names = ("init", "seeds", "expand", "resolve", "score", "pool", "frontier", "output")
-            tot = float(out[2:].sum())
-            d["phase_share"] = {k: round(float(v) / tot, 4) for k, v in zip(names, out[2:])}
+            tot = float(out[2:10].sum())
+            d["phase_share"] = {k: round(float(v) / tot, 4) for k, v in zip(names, out[2:10])}
+            if out[10:15].any():
+                sub = ("tc_gather", "tc_mma0", "tc_epi0", "tc_mma1", "tc_epi1")
+                d["score_sub_share"] = {k: round(float(v) / tot, 4) for k, v in zip(sub, out[10:15])}
         return d

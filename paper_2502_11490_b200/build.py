@@ -10,7 +10,6 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmpgr.so")
 SOURCES = ["gmpgr.cu"]
-HEADERS = ["common.cuh", "mlp_exact.cuh", "select.cuh", "search_kernel.cuh", "aux_kernels.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
@@ -24,7 +23,9 @@ def _stale() -> bool:
     if not os.path.exists(LIB):
         return True
     t = os.path.getmtime(LIB)
-    deps = [os.path.join(CSRC, f) for f in SOURCES + HEADERS]
+    import glob
+
+    deps = [os.path.join(CSRC, f) for f in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh"))
     deps.append(os.path.join(os.path.dirname(HERE), "include", "gmpgr.h"))
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 

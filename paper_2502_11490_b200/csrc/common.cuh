@@ -80,6 +80,7 @@ struct DevModel {
     const void *tcB;             // bf16 hi/lo core-matrix images: W0 item half, W1
     const float *tcMisc;         // b1[64] | W2[Z][64] | b2[4] | attention[4]
     int tc_ok;
+    const void *exBlock;         // exact weight block in FixedMlp/ExactQ layout (fixed shapes)
 };
 
 // Device graph: layer 0 as fixed-width rows padded with -1 (no count reads);

@@ -102,7 +102,7 @@ struct gr_model {
     int device;
     DevModel dm;
     void *dbuf;
-    void *tcbuf[2] = {nullptr, nullptr};
+    void *tcbuf[3] = {nullptr, nullptr, nullptr};
     std::vector<int> dims;
 };
 
@@ -236,6 +236,22 @@ int gr_model_create(int device, int n_mlp, const int32_t *dims, const float *con
         dm.tcB = dimg;
         dm.tcMisc = dmisc;
         dm.tc_ok = 1;
+        // exact weight block (FixedMlp / ExactQ layout): W0 item half, W1, W2, A, b0, b1, b2
+        const int pre = 4 * (dh / 16), nch0 = n_chunks(2 * dh), nchz = n_chunks(Z);
+        std::vector<float> ex;
+        auto put4 = [&](const float *src, size_t nf4) { ex.insert(ex.end(), src, src + nf4 * 4); };
+        put4(host.data() + offW[0] + (size_t)pre * 64 * 4, (size_t)(nch0 - pre) * 64);
+        put4(host.data() + offW[1], (size_t)16 * 64);
+        put4(host.data() + offW[2], (size_t)16 * Z);
+        put4(host.data() + offA, (size_t)nchz);
+        put4(host.data() + offb[0], 16);
+        put4(host.data() + offb[1], 16);
+        put4(host.data() + offb[2], (size_t)nchz);
+        float *dex = nullptr;
+        if (dmalloc(&dex, ex.size())) { cudaFree(d); delete M; return GR_ENOMEM; }
+        cudaMemcpy(dex, ex.data(), ex.size() * 4, cudaMemcpyHostToDevice);
+        M->tcbuf[2] = dex;
+        dm.exBlock = dex;
     }
     dm.n_mlp = n_mlp;
     dm.relu = relu ? 1 : 0;
@@ -258,6 +274,7 @@ int gr_model_destroy(gr_model *m) {
     cudaFree(m->dbuf);
     if (m->tcbuf[0]) cudaFree(m->tcbuf[0]);
     if (m->tcbuf[1]) cudaFree(m->tcbuf[1]);
+    if (m->tcbuf[2]) cudaFree(m->tcbuf[2]);
     delete m;
     return GR_OK;
 }
@@ -626,20 +643,20 @@ int check_params(const gr_search_params *p) {
     return GR_OK;
 }
 
-template <int DH, int ZZ, int MODE>
+template <int DH, int ZZ, int MODE, int NT, int G, int KC>
 int plan_mq(int k, int kp, SearchArgs &a) {
-    using EX = ExactQ<DH, ZZ>;
-    using TC = TcQ<DH, ZZ>;
+    using EX = ExactQ<DH, ZZ, NT / 32>;
+    using TC = TcQ<DH, ZZ, NT, G, KC>;
     SmemPlan P;
-    a.off_w0 = P.alloc(EX::W_END * 16);
+    a.off_w0 = NT >= 512 ? P.alloc(EX::W_END * 16) : 0;
     a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
     a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
-    a.off_acc0 = P.alloc(mq::G * 64 * 16);
-    a.off_hist = P.alloc(mq::NW * 256 * 4);
+    a.off_acc0 = P.alloc(G * 64 * 16);
+    a.off_hist = P.alloc((NT / 32) * 256 * 4);
     a.sortcap = pow2ceil(std::max(k, kp));
-    a.off_sortk = P.alloc(mq::G * a.sortcap * 8);
-    a.off_sortv = P.alloc(mq::G * a.sortcap * 4);
-    a.off_kp = P.alloc(3 * mq::G * kp * 4);
+    a.off_sortk = P.alloc(G * a.sortcap * 8);
+    a.off_sortv = P.alloc(G * a.sortcap * 4);
+    a.off_kp = P.alloc(3 * G * kp * 4);
     return P.bytes;
 }
 
@@ -650,12 +667,24 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
     const int mode = p->mode;
-    int smem = 0;
+    // one 512-thread CTA per SM, 4 queries (GMPGR_MQ=256: two 256-thread CTAs, 2 queries
+    // each, tensor-core mode only -- measured slower on cfg3: 854 vs 590 ms per 65k queries)
+    const char *menv = getenv("GMPGR_MQ");
+    const bool wide = mode != GR_MODE_TC || !(menv && std::strcmp(menv, "256") == 0);
+    int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? 4 : 2;
     void (*kern)(const SearchArgs) = nullptr;
-#define GR_MQ_CASE(CODE, DH, ZZ)                                                        \
-    case CODE:                                                                          \
-        if (mode == GR_MODE_TC) { smem = plan_mq<DH, ZZ, 1>(p->k, p->k_parallel, a); kern = hipanns_mq_kernel<DH, ZZ, 1>; } \
-        else { smem = plan_mq<DH, ZZ, 0>(p->k, p->k_parallel, a); kern = hipanns_mq_kernel<DH, ZZ, 0>; } \
+#define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \
+    case CODE:                                                                                     \
+        if (mode == GR_MODE_TC && wide) {                                                          \
+            smem = plan_mq<DH, ZZ, 1, 512, 4, DH>(p->k, p->k_parallel, a);                         \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 4, DH>;                                       \
+        } else if (mode == GR_MODE_TC) {                                                           \
+            smem = plan_mq<DH, ZZ, 1, 256, 2, 64>(p->k, p->k_parallel, a);                         \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 256, 2, 64>;                                       \
+        } else {                                                                                   \
+            smem = plan_mq<DH, ZZ, 0, 512, 4, DH>(p->k, p->k_parallel, a);                         \
+            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 4, DH>;                                       \
+        }                                                                                          \
         break;
     switch (shape) {
         GR_MQ_CASE(1283, 128, 3)
@@ -665,17 +694,18 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     default: return -1;
     }
 #undef GR_MQ_CASE
+    const int G_ = gq;
     if (smem > kMaxSmem) return -1;
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 0;
-    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, mq::NT, smem));
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, nthreads, smem));
     if (per_sm < 1) return -1;
-    const int64_t blocks = std::min<int64_t>((Q + mq::G - 1) / mq::G, (int64_t)per_sm * num_sms(G->device));
+    const int64_t blocks = std::min<int64_t>((Q + G_ - 1) / G_, (int64_t)per_sm * num_sms(G->device));
     const int64_t capF = (int64_t)p->k_parallel * p->ef;
     int64_t capS = std::min<int64_t>(capF * G->max_deg, (int64_t)p->k_parallel * G->dg.n);
     capS = std::max<int64_t>(capS, G->max_deg + 1) + 64;
     const int64_t capP = p->k + capS;
-    if (int rc = ensure_search_scratch(S, G, blocks * mq::G, capF, capS, capP)) return rc;
+    if (int rc = ensure_search_scratch(S, G, blocks * G_, capF, capS, capP)) return rc;
     a.g = G->dg;
     a.M = M->dm;
     a.it = I->di;
@@ -707,13 +737,13 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     a.phase_cycles = S->phase;
     a.band_rel = p->band_rel > 0.f ? p->band_rel : 1e-3f;
     a.band_abs = p->band_abs > 0.f ? p->band_abs : 1e-3f;
-    a.capF = S->capF * mq::G;  // CTA-level flattened lists
-    a.capS = S->capS * mq::G;
+    a.capF = S->capF * G_;  // CTA-level flattened lists
+    a.capS = S->capS * G_;
     a.capP = S->capP;          // per-query pools
     a.queue = S->flags;
     a.nonfinite = S->flags + 1;
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
-    kern<<<(int)blocks, mq::NT, smem, stream>>>(a);
+    kern<<<(int)blocks, nthreads, smem, stream>>>(a);
     GR_CUDA(cudaGetLastError());
     S->launches += 1;
     return GR_OK;
@@ -875,7 +905,7 @@ int gr_searcher_create(int device, gr_searcher **out) {
     cudaMemset(S->counters, 0, 16);
     const char *pt = getenv("GMPGR_PHASE_TIMING");
     if (pt && pt[0] == '1') {
-        if (dmalloc(&S->phase, 8) == GR_OK) cudaMemset(S->phase, 0, 64);
+        if (dmalloc(&S->phase, 16) == GR_OK) cudaMemset(S->phase, 0, 128);
     }
     *out = S;
     return GR_OK;
@@ -904,7 +934,7 @@ int gr_searcher_counters(gr_searcher *s, int64_t *out) {
     GR_CUDA(cudaSetDevice(s->device));
     GR_CUDA(cudaDeviceSynchronize());
     GR_CUDA(cudaMemcpy(out, s->counters, 16, cudaMemcpyDeviceToHost));
-    if (s->phase) GR_CUDA(cudaMemcpy(out + 2, s->phase, 64, cudaMemcpyDeviceToHost));
+    if (s->phase) GR_CUDA(cudaMemcpy(out + 2, s->phase, 128, cudaMemcpyDeviceToHost));
     return GR_OK;
 }
 

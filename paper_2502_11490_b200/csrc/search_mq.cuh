@@ -16,20 +16,15 @@
 #include "select.cuh"
 #include "tc_scorer.cuh"
 
-namespace mq {
-#ifndef GR_MQ_G
-#define GR_MQ_G 4
-#endif
-constexpr int NT = 512, NW = NT / 32, G = GR_MQ_G, GT = NT / G; // group threads for per-query sorts
-constexpr int PT = 4 * NW;                                   // exact tile: 64 pairs
-}  // namespace mq
+// launch shapes: (NT threads, G queries per CTA).  512x4: one CTA per SM with every
+// weight resident; 256x2: two CTAs per SM (tensor-core mode), exact weights read through L1.
 
 // Exact fixed-shape MLP on 64-pair tiles whose pairs may belong to different queries
 // (per-pair hoisted user half acc0[g]).  Same arithmetic as FixedMlp (bit-exact order).
-template <int D_H, int Z>
+template <int D_H, int Z, int NW>
 struct ExactQ {
     static constexpr int H = 64, NCH0 = D_H / 4, NCHH = H / 4, NCHZ = (Z + 3) / 4;
-    static constexpr int LDX0 = NCH0 | 1, LDH = NCHH | 1, LDZ = NCHZ | 1, PT = mq::PT;
+    static constexpr int LDX0 = NCH0 | 1, LDH = NCHH | 1, LDZ = NCHZ | 1, PT = 4 * NW;
     // float4 offsets of the weight block (same layout as FixedMlp) ...
     static constexpr int OFF_W0 = 0;
     static constexpr int OFF_W1 = OFF_W0 + NCH0 * H;
@@ -135,30 +130,34 @@ struct ExactQ {
 };
 
 // tcgen05 scorer for 512-thread CTAs: 128-pair tiles, per-pair query user half.
-template <int D_H, int Z>
+template <int D_H, int Z, int NT, int G, int KC_ = D_H>
 struct TcQ {
-    // layer 0 in ONE K chunk (A = 128 x D_H hi/lo = 64 KB at d_h 128, inside the exact
-    // activation buffers it aliases) -> two MMA round trips per tile
-    static constexpr int H = 64, TM = 128, KC = D_H, NKC0 = 1;
+    // layer 0 in D_H / KC K-chunks (KC = D_H: one chunk, A = 128 x D_H hi/lo = 64 KB at
+    // d_h 128 -> two MMA round trips per tile; KC = 64 halves the A buffer)
+    static constexpr int H = 64, TM = 128, KC = KC_, NKC0 = D_H / KC_;
+    static constexpr int NW = NT / 32, CQ = NW / 4, CW = H / CQ; // column groups / width
     static constexpr int OFF_B0H = 0;
     static constexpr int OFF_B0L = OFF_B0H + H * D_H * 2;
     static constexpr int OFF_B1H = OFF_B0L + H * D_H * 2;
     static constexpr int OFF_B1L = OFF_B1H + H * H * 2;
     static constexpr int A_BYTES = 2 * TM * KC * 2;       // A operand (hi, lo): caller-provided
     static constexpr int OFF_U = OFF_B1L + H * H * 2;     // [G][64] f32 user half + b0
-    static constexpr int OFF_B1 = OFF_U + mq::G * H * 4;
+    static constexpr int OFF_B1 = OFF_U + G * H * 4;
     static constexpr int OFF_W2 = OFF_B1 + H * 4;         // [Z][64]
     static constexpr int OFF_B2 = OFF_W2 + Z * H * 4;
     static constexpr int OFF_ATT = OFF_B2 + 16;
-    static constexpr int OFF_ZP = OFF_ATT + 16;           // [128][4][Z]
-    static constexpr int OFF_SC = OFF_ZP + TM * 4 * Z * 4;
+    static constexpr int OFF_ZP = OFF_ATT + 16;           // [128][CQ][Z]
+    static constexpr int OFF_SC = OFF_ZP + TM * CQ * Z * 4;
     static constexpr int OFF_PQ = OFF_SC + TM * 4;        // [128] query slot per row
     static constexpr int OFF_BAR = (OFF_PQ + TM * 4 + 15) & ~15;
     static constexpr int OFF_TMEM = OFF_BAR + 16;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr uint32_t IDESC = tc::idesc(TM, H);
 
-    static __device__ __forceinline__ void tmem_ld16(uint32_t addr, float (&v)[16]) {
+    static __device__ __forceinline__ void tmem_ldw(uint32_t addr, float (&v)[32]) {
+        tc::tmem_ld32(addr, v);
+    }
+    static __device__ __forceinline__ void tmem_ldw(uint32_t addr, float (&v)[16]) {
         uint32_t r[16];
         asm volatile(
             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
@@ -175,15 +174,24 @@ struct TcQ {
     // rows: slots[0..nv), query slot per row in PQ (written by the caller)
     static __device__ __forceinline__ void tile(unsigned char *sm, unsigned char *abuf, uint32_t tmem,
                                                 uint32_t &phase, const DevItems &it,
-                                                const DevGraph &g, const int32_t *slots, int nv) {
+                                                const DevGraph &g, const int32_t *slots, int nv,
+                                                unsigned long long *sub = nullptr) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        long long t_sub = (sub && tid == 0) ? clock64() : 0;
+        auto SUB = [&](int i) {
+            if (sub && tid == 0) { const long long n_ = clock64(); sub[i] += n_ - t_sub; t_sub = n_; }
+        };
         unsigned char *Ah = abuf, *Al = abuf + TM * KC * 2;
         uint64_t *bar = reinterpret_cast<uint64_t *>(sm + OFF_BAR);
         const uint32_t aH = tc::smem_u32(Ah), aL = tc::smem_u32(Al);
         for (int kc = 0; kc < NKC0; ++kc) {
             constexpr int CPR = KC / 4; // float4 per row chunk
-            for (int t = tid; t < TM * CPR; t += mq::NT) {
-                const int r = t / CPR, c = t % CPR;
+            // warp unit = 8 rows x 4 float4: the 8-byte hi/lo stores of a warp then cover
+            // two whole 128-byte core-matrix rows -> conflict-free (row-major mapping would
+            // put 16 lanes on one bank group); global reads stay 64-byte row segments
+            for (int t = tid; t < TM * CPR; t += NT) {
+                const int u = t >> 5, l = t & 31;
+                const int r = (u % (TM / 8)) * 8 + (l & 7), c = (u / (TM / 8)) * 4 + (l >> 3);
                 if (r < nv) {
                     const float4 x = __ldg(reinterpret_cast<const float4 *>(
                                                it.emb + slot_row(g, slots[r]) * it.ld) + kc * CPR + c);
@@ -197,6 +205,7 @@ struct TcQ {
             tc::fence_async_smem();
             tc::fence_before();
             __syncthreads();
+            SUB(0);
             if (tid == 0) {
                 tc::fence_after();
                 const uint32_t bH = tc::smem_u32(sm + OFF_B0H), bL = tc::smem_u32(sm + OFF_B0L);
@@ -214,16 +223,17 @@ struct TcQ {
             tc::mbar_wait(bar, phase);
             phase ^= 1u;
             tc::fence_after();
+            SUB(1);
         }
         const int q4 = warp & 3, cq = warp >> 2, row = q4 * 32 + lane;
         const int gq = reinterpret_cast<const int *>(sm + OFF_PQ)[row];
         const float *u = reinterpret_cast<const float *>(sm + OFF_U) + gq * H;
         {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + cq * 16, v);
+            float v[CW];
+            tmem_ldw(tmem + ((uint32_t)(q4 * 32) << 16) + cq * CW, v);
 #pragma unroll
-            for (int j = 0; j < 16; j += 4) {
-                const int o = cq * 16 + j;
+            for (int j = 0; j < CW; j += 4) {
+                const int o = cq * CW + j;
                 float4 y = make_float4(fmaxf(v[j] + u[o], 0.f), fmaxf(v[j + 1] + u[o + 1], 0.f),
                                        fmaxf(v[j + 2] + u[o + 2], 0.f), fmaxf(v[j + 3] + u[o + 3], 0.f));
                 uint2 hi, lo;
@@ -236,6 +246,7 @@ struct TcQ {
         tc::fence_async_smem();
         tc::fence_before();
         __syncthreads();
+        SUB(2);
         if (tid == 0) {
             tc::fence_after();
             const uint32_t bH = tc::smem_u32(sm + OFF_B1H), bL = tc::smem_u32(sm + OFF_B1L);
@@ -252,23 +263,24 @@ struct TcQ {
         tc::mbar_wait(bar, phase);
         phase ^= 1u;
         tc::fence_after();
+        SUB(3);
         {
-            float v[16];
-            tmem_ld16(tmem + ((uint32_t)(q4 * 32) << 16) + 64 + cq * 16, v);
+            float v[CW];
+            tmem_ldw(tmem + ((uint32_t)(q4 * 32) << 16) + 64 + cq * CW, v);
             const float *b1 = reinterpret_cast<const float *>(sm + OFF_B1);
             const float *W2 = reinterpret_cast<const float *>(sm + OFF_W2);
             float zp[Z];
 #pragma unroll
             for (int o = 0; o < Z; ++o) zp[o] = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                const float h = fmaxf(v[j] + b1[cq * 16 + j], 0.f);
+            for (int j = 0; j < CW; ++j) {
+                const float h = fmaxf(v[j] + b1[cq * CW + j], 0.f);
 #pragma unroll
-                for (int o = 0; o < Z; ++o) zp[o] = fmaf(h, W2[o * H + cq * 16 + j], zp[o]);
+                for (int o = 0; o < Z; ++o) zp[o] = fmaf(h, W2[o * H + cq * CW + j], zp[o]);
             }
             float *ZP = reinterpret_cast<float *>(sm + OFF_ZP);
 #pragma unroll
-            for (int o = 0; o < Z; ++o) ZP[(row * 4 + cq) * Z + o] = zp[o];
+            for (int o = 0; o < Z; ++o) ZP[(row * CQ + cq) * Z + o] = zp[o];
         }
         tc::fence_before();
         __syncthreads();
@@ -279,15 +291,20 @@ struct TcQ {
             float s = 0.f;
 #pragma unroll
             for (int o = 0; o < Z; ++o) {
-                const float z = ((ZP[(tid * 4) * Z + o] + ZP[(tid * 4 + 1) * Z + o]) +
-                                 (ZP[(tid * 4 + 2) * Z + o] + ZP[(tid * 4 + 3) * Z + o])) + b2[o];
+                float z = b2[o];
+#pragma unroll
+                for (int c = 0; c < CQ; ++c) z += ZP[(tid * CQ + c) * Z + o];
                 s = fmaf(z, att[o], s);
             }
             reinterpret_cast<float *>(sm + OFF_SC)[tid] = s;
         }
         __syncthreads();
+        SUB(4);
     }
 };
+
+template <int G>
+struct MqState;
 
 struct MqQuery {
     int q;             // global query index, -1 if this slot is idle
@@ -299,25 +316,27 @@ struct MqQuery {
     int64_t rows, nbrs;
 };
 
+template <int G>
 struct MqState {
-    MqQuery qs[mq::G];
-    int nF, nS, nFresh, nFn, nRq, f_cur, base, wrap[mq::G];
+    MqQuery qs[G];
+    int nF, nS, nFresh, nFn, nRq, f_cur, base, wrap[G];
     uint32_t bcast[4];
 };
 
 // Shared-memory plan (host computes the same offsets): [model block][exact buffers]
 // [hist NW x 256][sort G x sortcap keys+vals][seg cnt/off/fn: 3 x G*kp][acc0 G x 64 float4]
-template <int DH, int ZZ, int MODE>
-__global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs a) {
-    using EX = ExactQ<DH, ZZ>;
-    using TC = TcQ<DH, ZZ>;
-    constexpr int G = mq::G, NT = mq::NT, NW = mq::NW;
+template <int DH, int ZZ, int MODE, int NT, int G, int KC>
+__global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(const SearchArgs a) {
+    constexpr int NW = NT / 32, GT = NT / G;
+    constexpr bool W_SMEM = (NT >= 512);  // exact weight block in smem, else the global image
+    using EX = ExactQ<DH, ZZ, NW>;
+    using TC = TcQ<DH, ZZ, NT, G, KC>;
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ MqState st;
-    __shared__ unsigned long long ph_acc[8];
+    __shared__ MqState<G> st;
+    __shared__ unsigned long long ph_acc[16];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     long long ph_t0 = 0;
-    if (tid < 8) ph_acc[tid] = 0;
+    if (tid < 16) ph_acc[tid] = 0;
 #define GR_PH(i)                                                          \
     do {                                                                  \
         if (a.phase_cycles && tid == 0) {                                 \
@@ -329,7 +348,8 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
     const DevModel &M = a.M;
     const DevGraph &g = a.g;
     // ---- shared memory carve (offsets from the host plan)
-    float4 *sW = reinterpret_cast<float4 *>(smem + a.off_w0);      // exact weight block
+    const float4 *sW = W_SMEM ? reinterpret_cast<const float4 *>(smem + a.off_w0)
+                              : reinterpret_cast<const float4 *>(M.exBlock); // exact weights
     float4 *sBuf = reinterpret_cast<float4 *>(smem + a.off_x0);    // exact activation buffers
     float4 *sAcc0 = reinterpret_cast<float4 *>(smem + a.off_acc0); // [G][64]
     uint32_t *hist = reinterpret_cast<uint32_t *>(smem + a.off_hist);
@@ -340,16 +360,10 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
     int32_t *seg_off = seg_cnt + NSEG;
     int32_t *fn_off = seg_off + NSEG;
     // ---- exact weights (both modes: the tensor-core mode re-scores near thresholds)
-    {
-        const int O0 = 64, pre = M.pre_ch;
-        for (int t = tid; t < EX::NCH0 * O0; t += NT) sW[EX::OFF_W0 + t] = M.W[0][pre * O0 + t];
-        for (int t = tid; t < EX::NCHH * 64; t += NT) sW[EX::OFF_W1 + t] = M.W[1][t];
-        for (int t = tid; t < EX::NCHH * ZZ; t += NT) sW[EX::OFF_W2 + t] = M.W[2][t];
-        for (int t = tid; t < EX::NCHZ; t += NT) sW[EX::OFF_A + t] = M.A[t];
-        float *b0 = reinterpret_cast<float *>(sW + EX::OFF_B0), *b1 = reinterpret_cast<float *>(sW + EX::OFF_B1),
-              *b2 = reinterpret_cast<float *>(sW + EX::OFF_B2);
-        for (int t = tid; t < 64; t += NT) { b0[t] = M.b[0][t]; b1[t] = M.b[1][t]; }
-        for (int t = tid; t < 4 * EX::NCHZ; t += NT) b2[t] = t < ZZ ? M.b[2][t] : 0.f;
+    if constexpr (W_SMEM) {
+        float4 *sWm = reinterpret_cast<float4 *>(smem + a.off_w0);
+        const float4 *src = reinterpret_cast<const float4 *>(M.exBlock);
+        for (int t = tid; t < EX::W_END; t += NT) sWm[t] = src[t];
     }
     uint32_t tmem = 0, tphase = 0;
     unsigned char *tcs = smem + a.off_A; // tensor-core block (MODE 1)
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
                     if (tid < TC::TM) pq[tid] = tid < nv ? (fr_i[base + tid] >> 16) : 0;
                     __syncthreads();
                     TC::tile(tcs, reinterpret_cast<unsigned char *>(sBuf), tmem, tphase, a.it, g,
-                             fr_v + base, nv);
+                             fr_v + base, nv, a.phase_cycles ? ph_acc + 8 : nullptr);
                     if (tid < nv) {
                         const int gi = fr_i[base + tid], gq = gi >> 16;
                         const int32_t s = fr_v[base + tid];
@@ -571,7 +585,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         // per-query pool compaction to top-k (warp gq), tensor mode refines the band first
         auto compact_pools = [&]() {
             if constexpr (MODE == 1) {
-                __shared__ float thr[mq::G];
+                __shared__ float thr[G];
                 if (warp < G) {
                     const MqQuery &Q = st.qs[warp];
                     float Ts = INFINITY;
@@ -636,13 +650,13 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         };
         // sort each query's pool (group of GT threads per query, named barrier 1 + gq)
         auto sort_pools = [&]() {
-            const int gq = tid / mq::GT, gt = tid % mq::GT;
+            const int gq = tid / GT, gt = tid % GT;
             const MqQuery &Q = st.qs[gq];
             uint64_t *sk = sortk + gq * a.sortcap;
             int32_t *sv = sortv + gq * a.sortcap;
             const int np = Q.nPool;
-            for (int i = gt; i < np; i += mq::GT) { sk[i] = pkey(gq, Q.pool_cur)[i]; sv[i] = i; }
-            group_sort_desc<mq::GT>(sk, sv, np, a.sortcap, gt, 1 + gq);
+            for (int i = gt; i < np; i += GT) { sk[i] = pkey(gq, Q.pool_cur)[i]; sv[i] = i; }
+            group_sort_desc<GT>(sk, sv, np, a.sortcap, gt, 1 + gq);
             __syncthreads();
         };
 
@@ -684,7 +698,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         for (int layer = top; layer >= 0; --layer) {
             // ---- seeds: each query's pool sorted, first min(kp, |pool|) (exact in MODE 1)
             if constexpr (MODE == 1) {
-                __shared__ float thr2[mq::G];
+                __shared__ float thr2[G];
                 if (warp < G) {
                     const MqQuery &Q = st.qs[warp];
                     float Ts = -INFINITY;  // all entries when |pool| <= kp
@@ -891,7 +905,7 @@ __global__ void __launch_bounds__(mq::NT, 1) hipanns_mq_kernel(const SearchArgs 
         }
         GR_PH(7);
     }
-    if (a.phase_cycles && tid < 8) atomicAdd(a.phase_cycles + tid, ph_acc[tid]);
+    if (a.phase_cycles && tid < 16) atomicAdd(a.phase_cycles + tid, ph_acc[tid]);
 #undef GR_PH
     if constexpr (MODE == 1) {
         tc::fence_before();

@@ -152,7 +152,9 @@ struct TcMlp {
         // ---- layer 0: D0 = x_item . W0_item^T over NKC0 chunks of 64
         for (int kc = 0; kc < NKC0; ++kc) {
             for (int t = tid; t < TM * 16; t += GR_NT) {
-                const int r = t >> 4, c = t & 15;
+                // 8 rows x 4 float4 per warp: conflict-free core-matrix stores
+                const int u = t >> 5, l = t & 31;
+                const int r = (u % (TM / 8)) * 8 + (l & 7), c = (u / (TM / 8)) * 4 + (l >> 3);
                 if (r < nv) {
                     const int32_t s = slots[r];
                     const float4 x = __ldg(reinterpret_cast<const float4 *>(it.emb + slot_row(g, s) * it.ld) + kc * 16 + c);
