@@ -338,15 +338,23 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     mlp_tile(M, S, sWm, sbm, sA, sW0, x0_nch, pre > 0 ? sAcc0 : nullptr, nv,
                              a.nonfinite);
                 __syncthreads();
-                if (tid < nv) {
-                    const int32_t s = fr_v[base + tid];
-                    const uint64_t key = make_key(S.score[tid], slot_rank(g, s));
+                if (tid < 32) {  // nv <= GR_PT = 32: warp 0 holds the tile
+                    const int32_t s = tid < nv ? fr_v[base + tid] : 0;
+                    const uint64_t key = tid < nv ? make_key(S.score[tid], slot_rank(g, s)) : 0ull;
+                    uint64_t mx = key;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const uint64_t y = __shfl_xor_sync(0xffffffffu, mx, o);
+                        mx = y > mx ? y : mx;
+                    }
+                    if (tid == 0 && mx > st.hopmax) st.hopmax = mx;
+                    if (tid < nv) {
                     fr_key[base + tid] = key;
-                    atomicMax(reinterpret_cast<unsigned long long *>(&st.hopmax), key);
                     if (key > poolT) {
                         const int idx = atomicAdd(&st.nPool, 1);
                         pkey[pc][idx] = key;
                         pslot[pc][idx] = s;
+                    }
                     }
                 }
             }
@@ -543,40 +551,41 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                 const int fc = st.f_cur;
                 if (tid == 0) { st.nS = 0; st.nFresh = 0; }
                 __syncthreads();
-                // ---- expand + claim (4 frontier rows in flight per warp)
-                for (int e0 = warp * 4; e0 < nF; e0 += GR_NW * 4) {
-                    int32_t s[4], srch[4];
-                    const int32_t *row[4];
+                // ---- expand + claim: 8 frontier rows per warp; row loads, then all claim
+                // atomics back-to-back, then the ballots that consume them
+                constexpr int R = 8;
+                for (int e0 = warp * R; e0 < nF; e0 += GR_NW * R) {
+                    int32_t s[R], srch[R];
+                    const int32_t *row[R];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < R; ++u) {
                         const int e = e0 + u;
                         s[u] = e < nF ? fslot[fc][e] : -1;
                         srch[u] = e < nF ? fsrch[fc][e] : 0;
-                        row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
                     }
+#pragma unroll
+                    for (int u = 0; u < R; ++u) row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
                     int nvalid = 0;
                     for (int c0 = 0; c0 < deg; c0 += 32) {
-                        int32_t v[4];
+                        int32_t v[R];
+                        uint32_t old[R];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                        for (int u = 0; u < R; ++u)
                             v[u] = (row[u] && c0 + lane < deg) ? __ldg(row[u] + c0 + lane) : -1;
-                            nvalid += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
-                        }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            bool ok = false;
-                            if (v[u] >= 0) {
-                                const uint32_t code = claim_code(epoch, srch[u]);
-                                const uint32_t old = atomicMax(tags + v[u], code);
-                                ok = old < code;
-                            }
-                            warp_append2(ok, v[u], srch[u], &st.nS, surv_v, surv_i);
+                        for (int u = 0; u < R; ++u)
+                            old[u] = v[u] >= 0 ? atomicMax(tags + v[u], claim_code(epoch, srch[u])) : 0xFFFFFFFFu;
+#pragma unroll
+                        for (int u = 0; u < R; ++u) {
+                            nvalid += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
+                            warp_append2(v[u] >= 0 && old[u] < claim_code(epoch, srch[u]), v[u], srch[u],
+                                         &st.nS, surv_v, surv_i);
                         }
                     }
                     if (lane == 0) {
                         atomicAdd(reinterpret_cast<unsigned long long *>(&st.nbrs), (unsigned long long)nvalid);
                         atomicAdd(reinterpret_cast<unsigned long long *>(&st.rows),
-                                  (unsigned long long)min(4, nF - e0));
+                                  (unsigned long long)min(R, nF - e0));
                     }
                 }
                 __syncthreads();

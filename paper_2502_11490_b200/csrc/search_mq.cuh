@@ -175,7 +175,8 @@ struct TcQ {
     static __device__ __forceinline__ void tile(unsigned char *sm, unsigned char *abuf, uint32_t tmem,
                                                 uint32_t &phase, const DevItems &it,
                                                 const DevGraph &g, const int32_t *slots, int nv,
-                                                unsigned long long *sub = nullptr) {
+                                                unsigned long long *sub = nullptr,
+                                                const int32_t *next_slots = nullptr, int next_nv = 0) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         long long t_sub = (sub && tid == 0) ? clock64() : 0;
         auto SUB = [&](int i) {
@@ -219,6 +220,14 @@ struct TcQ {
                     tc::mma(tmem, al, bh, IDESC, 1u);
                 }
                 tc::commit(bar);
+            }
+            // while the tensor core works: pull the next tile's rows toward L2
+            if (kc == NKC0 - 1 && next_slots) {
+                constexpr int LPR = D_H / 32; // 128-byte lines per row
+                for (int t = tid; t < next_nv * LPR; t += NT) {
+                    const float *rp = it.emb + slot_row(g, next_slots[t / LPR]) * it.ld + (t % LPR) * 32;
+                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
+                }
             }
             tc::mbar_wait(bar, phase);
             phase ^= 1u;
@@ -312,9 +321,19 @@ struct MqQuery {
     int nPool, nPool2, pool_cur, f_off, f_cnt;
     uint64_t poolT;
     int besthop;
-    int64_t per_layer[GR_MAX_LAYERS];
-    int64_t rows, nbrs;
+    // 32-bit counters: shared-memory 32-bit atomics are native (64-bit ones would CAS-loop
+    // under the 128-way contention of a tile epilogue)
+    int per_layer[GR_MAX_LAYERS];
+    int rows, nbrs;
 };
+
+// one atomic per group of lanes sharing the same query slot (whole warp must call)
+__device__ __forceinline__ void warp_count(int *addr, int gq, int inc, bool active) {
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!active) return;
+    const unsigned peers = __match_any_sync(act, gq);
+    if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(addr, inc * __popc(peers));
+}
 
 template <int G>
 struct MqState {
@@ -459,19 +478,24 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                 int *pq = reinterpret_cast<int *>(tcs + TC::OFF_PQ);
                 for (int base = 0; base < n; base += TC::TM) {
                     const int nv = min(TC::TM, n - base);
-                    if (tid < TC::TM) pq[tid] = tid < nv ? (fr_i[base + tid] >> 16) : 0;
-                    __syncthreads();
+                    int32_t my_s = 0;
+                    int my_gi = 0;
+                    if (tid < nv) { my_s = fr_v[base + tid]; my_gi = fr_i[base + tid]; }
+                    if (tid < TC::TM) pq[tid] = my_gi >> 16;  // read after the tile's first barrier
+                    const int nb = base + TC::TM;
                     TC::tile(tcs, reinterpret_cast<unsigned char *>(sBuf), tmem, tphase, a.it, g,
-                             fr_v + base, nv, a.phase_cycles ? ph_acc + 8 : nullptr);
+                             fr_v + base, nv, a.phase_cycles ? ph_acc + 8 : nullptr,
+                             nb < n ? fr_v + nb : nullptr, nb < n ? min(TC::TM, n - nb) : 0);
+                    if (tid < 32 * ((nv + 31) / 32))
+                        warp_count(&st.qs[my_gi >> 16].per_layer[layer], my_gi >> 16, 1, tid < nv);
                     if (tid < nv) {
-                        const int gi = fr_i[base + tid], gq = gi >> 16;
-                        const int32_t s = fr_v[base + tid];
+                        const int gi = my_gi, gq = gi >> 16;
+                        const int32_t s = my_s;
                         const float v = sc[tid];
                         if (!isfinite(v)) atomicOr(a.nonfinite, 1);
                         const uint64_t key = make_key(v, slot_rank(g, s));
                         fr_key[base + tid] = key;
                         MqQuery &Q = st.qs[gq];
-                        atomicAdd(reinterpret_cast<unsigned long long *>(&Q.per_layer[layer]), 1ull);
                         const float Ts = orderable_f32((uint32_t)(Q.poolT >> 32));
                         if (!Q.poolT || v >= Ts - band_of(Ts)) {
                             const int idx = atomicAdd(&Q.nPool, 1);
@@ -503,13 +527,17 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                     }
                     __syncthreads();
                     EX::tile(sW, sBuf, sAcc0, nv, a.nonfinite);
+                    {
+                        const int gq0 = tid < nv ? (fr_i[base + tid] >> 16) : 0;
+                        if (tid < 32 * ((nv + 31) / 32))
+                            warp_count(&st.qs[gq0].per_layer[layer], gq0, 1, tid < nv);
+                    }
                     if (tid < nv) {
                         const int gq = fr_i[base + tid] >> 16;
                         const int32_t s = fr_v[base + tid];
                         const uint64_t key = make_key(sc[tid], slot_rank(g, s));
                         fr_key[base + tid] = key;
                         MqQuery &Q = st.qs[gq];
-                        atomicAdd(reinterpret_cast<unsigned long long *>(&Q.per_layer[layer]), 1ull);
                         if (key > Q.poolT) {
                             const int idx = atomicAdd(&Q.nPool, 1);
                             pkey(gq, Q.pool_cur)[idx] = key;
@@ -743,44 +771,47 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                 const int fc = st.f_cur;
                 if (tid == 0) { st.nS = 0; st.nFresh = 0; }
                 __syncthreads();
-                // ---- expand + claim, 4 frontier rows in flight per warp
-                for (int e0 = warp * 4; e0 < nF; e0 += NW * 4) {
-                    int32_t s[4], gi[4];
-                    const int32_t *row[4];
+                // ---- expand + claim: 8 frontier rows per warp, all row loads then all claim
+                // atomics issued back-to-back (the ballots that consume them come after)
+                constexpr int R = 8;
+                for (int e0 = warp * R; e0 < nF; e0 += NW * R) {
+                    int32_t s[R], gi[R];
+                    const int32_t *row[R];
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < R; ++u) {
                         const int e = e0 + u;
                         s[u] = e < nF ? fslot[fc][e] : -1;
                         gi[u] = e < nF ? fsrch[fc][e] : 0;
-                        row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
                     }
-                    int nvalid[4] = {0, 0, 0, 0};
-                    for (int c0 = 0; c0 < deg; c0 += 32) {
-                        int32_t v[4];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < R; ++u) row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
+                    int nvalid[R];
+#pragma unroll
+                    for (int u = 0; u < R; ++u) nvalid[u] = 0;
+                    for (int c0 = 0; c0 < deg; c0 += 32) {
+                        int32_t v[R];
+                        uint32_t old[R], code[R];
+#pragma unroll
+                        for (int u = 0; u < R; ++u)
                             v[u] = (row[u] && c0 + lane < deg) ? __ldg(row[u] + c0 + lane) : -1;
-                            nvalid[u] += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
+#pragma unroll
+                        for (int u = 0; u < R; ++u) {
+                            code[u] = claim_code(st.qs[gi[u] >> 16].epoch, gi[u] & 0xFFFF);
+                            old[u] = v[u] >= 0 ? atomicMax(tags_of(gi[u] >> 16) + v[u], code[u]) : 0xFFFFFFFFu;
                         }
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            bool ok = false;
-                            if (v[u] >= 0) {
-                                const int gq = gi[u] >> 16;
-                                const uint32_t code = claim_code(st.qs[gq].epoch, gi[u] & 0xFFFF);
-                                const uint32_t old = atomicMax(tags_of(gq) + v[u], code);
-                                ok = old < code;
-                            }
-                            warp_append2(ok, v[u], gi[u], &st.nS, surv_v, surv_i);
+                        for (int u = 0; u < R; ++u) {
+                            nvalid[u] += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
+                            warp_append2(v[u] >= 0 && old[u] < code[u], v[u], gi[u], &st.nS, surv_v, surv_i);
                         }
                     }
                     if (lane == 0) {
 #pragma unroll
-                        for (int u = 0; u < 4; ++u)
+                        for (int u = 0; u < R; ++u)
                             if (s[u] >= 0) {
                                 MqQuery &Q = st.qs[gi[u] >> 16];
-                                atomicAdd(reinterpret_cast<unsigned long long *>(&Q.rows), 1ull);
-                                atomicAdd(reinterpret_cast<unsigned long long *>(&Q.nbrs), (unsigned long long)nvalid[u]);
+                                atomicAdd(&Q.rows, 1);
+                                atomicAdd(&Q.nbrs, nvalid[u]);
                             }
                     }
                 }

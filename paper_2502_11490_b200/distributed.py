@@ -41,6 +41,8 @@ def gather_lists(ids, scores, group=None):
     import torch
     import torch.distributed as dist
 
+    if not (dist.is_available() and dist.is_initialized()):
+        return ids[None], scores[None]  # single process: one shard
     world = dist.get_world_size(group)
     gi = [torch.empty_like(ids) for _ in range(world)]
     gs = [torch.empty_like(scores) for _ in range(world)]

@@ -72,3 +72,44 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     items_host = items.cpu().numpy() if host_items else None
     return Workload(name, model, items, items_host, np.ascontiguousarray(users, np.float32), index,
                     time.perf_counter() - t0)
+
+
+def make_shard(rank: int, world: int, shard_n: int = 12_500_000, d: int = 128, m: int = 24,
+               Z: int = 3, n_queries: int = 65_536, device: int = 0) -> Workload:
+    """BASELINE config 4: a catalog of shard_n * world items split in contiguous global-id
+    ranges; this rank's shard is an independent graph over items [rank*shard_n, ...) with
+    GLOBAL ids (slot order = id order) and local embedding rows.  Cluster centres and users
+    are shared by all ranks; per-shard items come from a rank-seeded stream."""
+    import torch
+
+    t0 = time.perf_counter()
+    dev = torch.device("cuda", device)
+    model = create_model(d_x=d, d_h=d, z_dim=Z, hidden=(64, 64), seed=1)
+    C = max(64, int(4096 * shard_n * world / 10_000_000))
+    g = torch.Generator(device=dev)
+    g.manual_seed(0)
+    centers = torch.randn(C, d, generator=g, device=dev) * 4.0
+    gs = torch.Generator(device=dev)
+    gs.manual_seed(1_000_003 * (rank + 1))
+    assign = torch.randint(0, C, (shard_n,), generator=gs, device=dev)
+    w_item = torch.from_numpy(model.item_projector.weight.astype(np.float32)).to(dev)
+    items = torch.empty((shard_n, d), dtype=torch.float32, device=dev)
+    prev = torch.backends.cuda.matmul.allow_tf32
+    torch.backends.cuda.matmul.allow_tf32 = False
+    for s0 in range(0, shard_n, 1 << 20):
+        e = min(shard_n, s0 + (1 << 20))
+        items[s0:e] = (centers[assign[s0:e]] + torch.randn(e - s0, d, generator=gs, device=dev)) @ w_item
+    gu = torch.Generator(device=dev)
+    gu.manual_seed(7)
+    w_user = torch.from_numpy(model.user_projector.weight.astype(np.float32)).to(dev)
+    users = (torch.randn(n_queries, d, generator=gu, device=dev) @ w_user).cpu().numpy()
+    torch.backends.cuda.matmul.allow_tf32 = prev
+    del centers, assign
+    lo = rank * shard_n
+    index = GraphIndex.build(items, ids=np.arange(lo, lo + shard_n, dtype=np.int64), m=m,
+                             seed=rank, device=dev)
+    index.rows = np.arange(shard_n, dtype=np.int32)
+    torch.cuda.synchronize(dev)
+    torch.cuda.empty_cache()
+    return Workload("cfg4", model, items, None, np.ascontiguousarray(users, np.float32), index,
+                    time.perf_counter() - t0)
