@@ -671,16 +671,25 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     // each, tensor-core mode only -- measured slower on cfg3: 854 vs 590 ms per 65k queries)
     const char *menv = getenv("GMPGR_MQ");
     const bool wide = mode != GR_MODE_TC || !(menv && std::strcmp(menv, "256") == 0);
-    int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? 4 : 2;
+    // 8 queries per CTA in lock-step (GMPGR_MQ_G=4 for 4): +6% on cfg3 in tc mode
+    const char *genv = getenv("GMPGR_MQ_G");
+    const bool g8 = !(genv && std::strcmp(genv, "4") == 0);
+    int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? (g8 ? 8 : 4) : 2;
     void (*kern)(const SearchArgs) = nullptr;
 #define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \
     case CODE:                                                                                     \
-        if (mode == GR_MODE_TC && wide) {                                                          \
+        if (mode == GR_MODE_TC && wide && g8) {                                                    \
+            smem = plan_mq<DH, ZZ, 1, 512, 8, DH>(p->k, p->k_parallel, a);                         \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH>;                                       \
+        } else if (mode == GR_MODE_TC && wide) {                                                   \
             smem = plan_mq<DH, ZZ, 1, 512, 4, DH>(p->k, p->k_parallel, a);                         \
             kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 4, DH>;                                       \
         } else if (mode == GR_MODE_TC) {                                                           \
             smem = plan_mq<DH, ZZ, 1, 256, 2, 64>(p->k, p->k_parallel, a);                         \
             kern = hipanns_mq_kernel<DH, ZZ, 1, 256, 2, 64>;                                       \
+        } else if (g8) {                                                                           \
+            smem = plan_mq<DH, ZZ, 0, 512, 8, DH>(p->k, p->k_parallel, a);                         \
+            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH>;                                       \
         } else {                                                                                   \
             smem = plan_mq<DH, ZZ, 0, 512, 4, DH>(p->k, p->k_parallel, a);                         \
             kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 4, DH>;                                       \

@@ -85,7 +85,7 @@ def make_shard(rank: int, world: int, shard_n: int = 12_500_000, d: int = 128, m
     t0 = time.perf_counter()
     dev = torch.device("cuda", device)
     model = create_model(d_x=d, d_h=d, z_dim=Z, hidden=(64, 64), seed=1)
-    C = max(64, int(4096 * shard_n * world / 10_000_000))
+    C = 4096  # n_clusters 4096 for configs 3 and 4
     g = torch.Generator(device=dev)
     g.manual_seed(0)
     centers = torch.randn(C, d, generator=g, device=dev) * 4.0
