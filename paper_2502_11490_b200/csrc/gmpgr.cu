@@ -643,14 +643,22 @@ int check_params(const gr_search_params *p) {
     return GR_OK;
 }
 
-template <int DH, int ZZ, int MODE, int NT, int G, int KC>
+template <int DH, int ZZ, int MODE, int NT, int G, int KC, bool PIPE = false>
 int plan_mq(int k, int kp, SearchArgs &a) {
     using EX = ExactQ<DH, ZZ, NT / 32>;
     using TC = TcQ<DH, ZZ, NT, G, KC>;
+    using TP = TcPipe<DH, ZZ, G>;
     SmemPlan P;
-    a.off_w0 = NT >= 512 ? P.alloc(EX::W_END * 16) : 0;
-    a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
-    a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
+    if (MODE == 1 && PIPE) {
+        static_assert(TP::A_REGION >= EX::BUF_END * 16 || !PIPE, "exact buffers must fit the A region");
+        a.off_w0 = 0;
+        a.off_A = P.alloc(TP::BYTES);
+        a.off_x0 = a.off_A + TP::OFF_A;  // exact re-scoring buffers alias the A region
+    } else {
+        a.off_w0 = NT >= 512 ? P.alloc(EX::W_END * 16) : 0;
+        a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
+        a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
+    }
     a.off_acc0 = P.alloc(G * 64 * 16);
     a.off_hist = P.alloc((NT / 32) * 256 * 4);
     a.sortcap = pow2ceil(std::max(k, kp));
@@ -674,25 +682,30 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     // 8 queries per CTA in lock-step (GMPGR_MQ_G=4 for 4): +6% on cfg3 in tc mode
     const char *genv = getenv("GMPGR_MQ_G");
     const bool g8 = !(genv && std::strcmp(genv, "4") == 0);
-    int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? (g8 ? 8 : 4) : 2;
+    const char *penv = getenv("GMPGR_PIPE");  // warp-specialised tcgen05 scoring pipeline
+    const bool pipe = penv && std::strcmp(penv, "1") == 0;
+    int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? ((g8 || (pipe && mode == GR_MODE_TC)) ? 8 : 4) : 2;
     void (*kern)(const SearchArgs) = nullptr;
 #define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \
     case CODE:                                                                                     \
-        if (mode == GR_MODE_TC && wide && g8) {                                                    \
+        if (mode == GR_MODE_TC && wide && pipe) {                                                  \
+            smem = plan_mq<DH, ZZ, 1, 512, 8, DH, true>(p->k, p->k_parallel, a);                   \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH, true>;                                 \
+        } else if (mode == GR_MODE_TC && wide && g8) {                                             \
             smem = plan_mq<DH, ZZ, 1, 512, 8, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH>;                                       \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH, false>;                                       \
         } else if (mode == GR_MODE_TC && wide) {                                                   \
             smem = plan_mq<DH, ZZ, 1, 512, 4, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 4, DH>;                                       \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 4, DH, false>;                                       \
         } else if (mode == GR_MODE_TC) {                                                           \
             smem = plan_mq<DH, ZZ, 1, 256, 2, 64>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 256, 2, 64>;                                       \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 256, 2, 64, false>;                                       \
         } else if (g8) {                                                                           \
             smem = plan_mq<DH, ZZ, 0, 512, 8, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH>;                                       \
+            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH, false>;                                       \
         } else {                                                                                   \
             smem = plan_mq<DH, ZZ, 0, 512, 4, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 4, DH>;                                       \
+            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 4, DH, false>;                                       \
         }                                                                                          \
         break;
     switch (shape) {

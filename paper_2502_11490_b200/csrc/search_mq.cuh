@@ -15,6 +15,7 @@
 #include "search_kernel.cuh"
 #include "select.cuh"
 #include "tc_scorer.cuh"
+#include "tc_pipe.cuh"
 
 // launch shapes: (NT threads, G queries per CTA).  512x4: one CTA per SM with every
 // weight resident; 256x2: two CTAs per SM (tensor-core mode), exact weights read through L1.
@@ -344,12 +345,22 @@ struct MqState {
 
 // Shared-memory plan (host computes the same offsets): [model block][exact buffers]
 // [hist NW x 256][sort G x sortcap keys+vals][seg cnt/off/fn: 3 x G*kp][acc0 G x 64 float4]
-template <int DH, int ZZ, int MODE, int NT, int G, int KC>
+template <int DH, int ZZ, int MODE, int NT, int G, int KC, bool PIPE>
 __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(const SearchArgs a) {
     constexpr int NW = NT / 32, GT = NT / G;
-    constexpr bool W_SMEM = (NT >= 512);  // exact weight block in smem, else the global image
+    // exact weight block in smem, else the global image (the pipelined scorer needs the room)
+    constexpr bool W_SMEM = (NT >= 512) && !(MODE == 1 && PIPE);
     using EX = ExactQ<DH, ZZ, NW>;
     using TC = TcQ<DH, ZZ, NT, G, KC>;
+    using TP = TcPipe<DH, ZZ, G>;
+    constexpr int OFF_U = PIPE ? TP::OFF_U : TC::OFF_U;
+    constexpr int OFF_B1 = PIPE ? TP::OFF_B1 : TC::OFF_B1;
+    constexpr int OFF_W2 = PIPE ? TP::OFF_W2 : TC::OFF_W2;
+    constexpr int OFF_B2 = PIPE ? TP::OFF_B2 : TC::OFF_B2;
+    constexpr int OFF_ATT = PIPE ? TP::OFF_ATT : TC::OFF_ATT;
+    constexpr int OFF_TMEMP = PIPE ? TP::OFF_TMEM : TC::OFF_TMEM;
+    constexpr uint32_t TMEM_COLS = PIPE ? TP::TMEM_COLS : 128;
+    uint32_t chunk_ctr = 0, tile_ctr = 0;  // pipelined scorer barrier phases
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ MqState<G> st;
     __shared__ unsigned long long ph_acc[16];
@@ -388,23 +399,24 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
     unsigned char *tcs = smem + a.off_A; // tensor-core block (MODE 1)
     if constexpr (MODE == 1) {
         const uint4 *src = reinterpret_cast<const uint4 *>(M.tcB);
-        uint4 *dst = reinterpret_cast<uint4 *>(tcs + TC::OFF_B0H);
+        uint4 *dst = reinterpret_cast<uint4 *>(tcs + TC::OFF_B0H);  // same B layout in TC and TP
         for (int t = tid; t < (TC::OFF_U - TC::OFF_B0H) / 16; t += NT) dst[t] = src[t];
-        float *b1 = reinterpret_cast<float *>(tcs + TC::OFF_B1);
+        float *b1 = reinterpret_cast<float *>(tcs + OFF_B1);
         for (int t = tid; t < 64; t += NT) b1[t] = M.tcMisc[t];
-        float *w2 = reinterpret_cast<float *>(tcs + TC::OFF_W2);
+        float *w2 = reinterpret_cast<float *>(tcs + OFF_W2);
         for (int t = tid; t < 64 * ZZ; t += NT) w2[t] = M.tcMisc[64 + t];
         if (tid < 4) {
-            reinterpret_cast<float *>(tcs + TC::OFF_B2)[tid] = M.tcMisc[64 + 64 * ZZ + tid];
-            reinterpret_cast<float *>(tcs + TC::OFF_ATT)[tid] = M.tcMisc[68 + 64 * ZZ + tid];
+            reinterpret_cast<float *>(tcs + OFF_B2)[tid] = M.tcMisc[64 + 64 * ZZ + tid];
+            reinterpret_cast<float *>(tcs + OFF_ATT)[tid] = M.tcMisc[68 + 64 * ZZ + tid];
         }
-        uint32_t *tptr = reinterpret_cast<uint32_t *>(tcs + TC::OFF_TMEM);
+        uint32_t *tptr = reinterpret_cast<uint32_t *>(tcs + OFF_TMEMP);
         if (warp == 0) {
             asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                             tc::smem_u32(tptr)), "r"(128));
+                             tc::smem_u32(tptr)), "r"(TMEM_COLS));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }
-        if (tid == 0) tc::mbar_init(reinterpret_cast<uint64_t *>(tcs + TC::OFF_BAR), 1);
+        if constexpr (PIPE) TP::init_barriers(tcs);
+        else if (tid == 0) tc::mbar_init(reinterpret_cast<uint64_t *>(tcs + TC::OFF_BAR), 1);
         tc::fence_before();
         __syncthreads();
         tc::fence_after();
@@ -467,13 +479,35 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
             }
             sAcc0[gq * 64 + o] = acc;
             if constexpr (MODE == 1)
-                reinterpret_cast<float *>(tcs + TC::OFF_U)[gq * 64 + o] = __fadd_rn(hsum4(acc), M.b[0][o]);
+                reinterpret_cast<float *>(tcs + OFF_U)[gq * 64 + o] = __fadd_rn(hsum4(acc), M.b[0][o]);
         }
 
         // ================= helpers
         // score fresh (fr_v, fr_i) [0, n): keys; per-query per-layer counts; pool append
         auto score_fresh = [&](int n, int layer, int hop) {
-            if constexpr (MODE == 1) {
+            if constexpr (MODE == 1 && PIPE) {
+                TP::run(tcs, tmem, a.it, g, fr_v, n, chunk_ctr, tile_ctr,
+                        [&](int i) { return fr_i[i] >> 16; },
+                        [&](int i, bool valid, float v) {
+                            const int gi = valid ? fr_i[i] : 0, gq = gi >> 16;
+                            warp_count(&st.qs[gq].per_layer[layer], gq, 1, valid);
+                            if (!valid) return;
+                            const int32_t s = fr_v[i];
+                            if (!isfinite(v)) atomicOr(a.nonfinite, 1);
+                            const uint64_t key = make_key(v, slot_rank(g, s));
+                            fr_key[i] = key;
+                            MqQuery &Q = st.qs[gq];
+                            const float Ts = orderable_f32((uint32_t)(Q.poolT >> 32));
+                            if (!Q.poolT || v >= Ts - band_of(Ts)) {
+                                const int idx = atomicAdd(&Q.nPool, 1);
+                                pkey(gq, Q.pool_cur)[idx] = key;
+                                pslot(gq, Q.pool_cur)[idx] = s;
+                                pmeta(gq, Q.pool_cur)[idx] = hop << 1;
+                            }
+                        });
+                if (tid == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
+                __syncthreads();
+            } else if constexpr (MODE == 1) {
                 const float *sc = reinterpret_cast<const float *>(tcs + TC::OFF_SC);
                 int *pq = reinterpret_cast<int *>(tcs + TC::OFF_PQ);
                 for (int base = 0; base < n; base += TC::TM) {
@@ -942,6 +976,6 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
         tc::fence_before();
         __syncthreads();
         if (warp == 0)
-            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
+            asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }
 }
