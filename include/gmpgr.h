@@ -115,7 +115,8 @@ int gr_score_items_approx(const gr_model *m, const gr_items *it, const float *us
 int gr_searcher_create(int device, gr_searcher **out);
 int gr_searcher_destroy(gr_searcher *s);
 
-/* Batched C-HiPANNS, deterministic lock-step semantics, exact fp32 scoring.
+/* Batched C-HiPANNS, deterministic lock-step semantics; results identical to the exact fp32
+ * scorer in both modes (see gr_search_params.mode).
  * users fp32 [Q, d_h].  Outputs: ids int64 [Q, k] (-1 padded), scores fp64 [Q, k],
  * count int32 [Q], stats int64 [Q, 5 + n_layers] = (metric_evaluations, nodes_visited,
  * hops_to_best or -1, adjacency rows expanded, neighbour ids read, per-layer evaluations

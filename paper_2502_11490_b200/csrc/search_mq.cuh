@@ -336,6 +336,22 @@ __device__ __forceinline__ void warp_count(int *addr, int gq, int inc, bool acti
     if ((int)(threadIdx.x & 31) == __ffs(peers) - 1) atomicAdd(addr, inc * __popc(peers));
 }
 
+// Warp-aggregated slot reservation: lanes with the same gq share one shared-memory atomic
+// (per-lane atomics on one query's pool counter serialise).  All 32 lanes must call.
+// Returns the lane's index, or -1 when !active.
+template <class CtrOf>
+__device__ __forceinline__ int warp_append(int gq, bool active, CtrOf ctr_of) {
+    const unsigned act = __ballot_sync(0xffffffffu, active);
+    if (!active) return -1;
+    const int lane = threadIdx.x & 31;
+    const unsigned peers = __match_any_sync(act, gq);
+    const int leader = __ffs(peers) - 1;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(ctr_of(gq), __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    return base + __popc(peers & ((1u << lane) - 1u));
+}
+
 template <int G>
 struct MqState {
     MqQuery qs[G];
@@ -486,25 +502,23 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
         // score fresh (fr_v, fr_i) [0, n): keys; per-query per-layer counts; pool append
         auto score_fresh = [&](int n, int layer, int hop) {
             if constexpr (MODE == 1 && PIPE) {
-                TP::run(tcs, tmem, a.it, g, fr_v, n, chunk_ctr, tile_ctr,
-                        [&](int i) { return fr_i[i] >> 16; },
-                        [&](int i, bool valid, float v) {
-                            const int gi = valid ? fr_i[i] : 0, gq = gi >> 16;
+                TP::run(tcs, tmem, a.it, g, fr_v, fr_i, n, chunk_ctr, tile_ctr,
+                        [&](int i, bool valid, float v, int gi, int32_t s) {
+                            const int gq = gi >> 16;
                             warp_count(&st.qs[gq].per_layer[layer], gq, 1, valid);
-                            if (!valid) return;
-                            const int32_t s = fr_v[i];
-                            if (!isfinite(v)) atomicOr(a.nonfinite, 1);
+                            if (valid && !isfinite(v)) atomicOr(a.nonfinite, 1);
                             const uint64_t key = make_key(v, slot_rank(g, s));
-                            fr_key[i] = key;
+                            if (valid) fr_key[i] = key;
                             MqQuery &Q = st.qs[gq];
                             const float Ts = orderable_f32((uint32_t)(Q.poolT >> 32));
-                            if (!Q.poolT || v >= Ts - band_of(Ts)) {
-                                const int idx = atomicAdd(&Q.nPool, 1);
+                            const int idx = warp_append(gq, valid && (!Q.poolT || v >= Ts - band_of(Ts)),
+                                                        [&](int q) { return &st.qs[q].nPool; });
+                            if (idx >= 0) {
                                 pkey(gq, Q.pool_cur)[idx] = key;
                                 pslot(gq, Q.pool_cur)[idx] = s;
                                 pmeta(gq, Q.pool_cur)[idx] = hop << 1;
                             }
-                        });
+                        }, a.phase_cycles ? ph_acc + 8 : nullptr);
                 if (tid == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
                 __syncthreads();
             } else if constexpr (MODE == 1) {
@@ -520,19 +534,20 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                     TC::tile(tcs, reinterpret_cast<unsigned char *>(sBuf), tmem, tphase, a.it, g,
                              fr_v + base, nv, a.phase_cycles ? ph_acc + 8 : nullptr,
                              nb < n ? fr_v + nb : nullptr, nb < n ? min(TC::TM, n - nb) : 0);
-                    if (tid < 32 * ((nv + 31) / 32))
-                        warp_count(&st.qs[my_gi >> 16].per_layer[layer], my_gi >> 16, 1, tid < nv);
-                    if (tid < nv) {
-                        const int gi = my_gi, gq = gi >> 16;
+                    if (tid < 32 * ((nv + 31) / 32)) {
+                        const bool valid = tid < nv;
+                        const int gq = my_gi >> 16;
+                        warp_count(&st.qs[gq].per_layer[layer], gq, 1, valid);
                         const int32_t s = my_s;
-                        const float v = sc[tid];
-                        if (!isfinite(v)) atomicOr(a.nonfinite, 1);
+                        const float v = valid ? sc[tid] : 0.f;
+                        if (valid && !isfinite(v)) atomicOr(a.nonfinite, 1);
                         const uint64_t key = make_key(v, slot_rank(g, s));
-                        fr_key[base + tid] = key;
+                        if (valid) fr_key[base + tid] = key;
                         MqQuery &Q = st.qs[gq];
                         const float Ts = orderable_f32((uint32_t)(Q.poolT >> 32));
-                        if (!Q.poolT || v >= Ts - band_of(Ts)) {
-                            const int idx = atomicAdd(&Q.nPool, 1);
+                        const int idx = warp_append(gq, valid && (!Q.poolT || v >= Ts - band_of(Ts)),
+                                                    [&](int q) { return &st.qs[q].nPool; });
+                        if (idx >= 0) {
                             pkey(gq, Q.pool_cur)[idx] = key;
                             pslot(gq, Q.pool_cur)[idx] = s;
                             pmeta(gq, Q.pool_cur)[idx] = hop << 1;
@@ -561,19 +576,17 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                     }
                     __syncthreads();
                     EX::tile(sW, sBuf, sAcc0, nv, a.nonfinite);
-                    {
-                        const int gq0 = tid < nv ? (fr_i[base + tid] >> 16) : 0;
-                        if (tid < 32 * ((nv + 31) / 32))
-                            warp_count(&st.qs[gq0].per_layer[layer], gq0, 1, tid < nv);
-                    }
-                    if (tid < nv) {
-                        const int gq = fr_i[base + tid] >> 16;
-                        const int32_t s = fr_v[base + tid];
-                        const uint64_t key = make_key(sc[tid], slot_rank(g, s));
-                        fr_key[base + tid] = key;
+                    if (tid < 32 * ((nv + 31) / 32)) {
+                        const bool valid = tid < nv;
+                        const int gq = valid ? (fr_i[base + tid] >> 16) : 0;
+                        warp_count(&st.qs[gq].per_layer[layer], gq, 1, valid);
+                        const int32_t s = valid ? fr_v[base + tid] : 0;
+                        const uint64_t key = make_key(valid ? sc[tid] : 0.f, slot_rank(g, s));
+                        if (valid) fr_key[base + tid] = key;
                         MqQuery &Q = st.qs[gq];
-                        if (key > Q.poolT) {
-                            const int idx = atomicAdd(&Q.nPool, 1);
+                        const int idx = warp_append(gq, valid && key > Q.poolT,
+                                                    [&](int q) { return &st.qs[q].nPool; });
+                        if (idx >= 0) {
                             pkey(gq, Q.pool_cur)[idx] = key;
                             pslot(gq, Q.pool_cur)[idx] = s;
                             pmeta(gq, Q.pool_cur)[idx] = (hop << 1) | 1;
@@ -863,7 +876,13 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                 for (int i = tid; i < NSEG; i += NT) seg_cnt[i] = 0;
                 __syncthreads();
                 auto seg_of = [&](int gi) { return (gi >> 16) * a.kp + (gi & 0xFFFF); };
-                for (int t2 = tid; t2 < nFresh; t2 += NT) atomicAdd(&seg_cnt[seg_of(fr_i[t2])], 1);
+                for (int t0 = 0; t0 < nFresh; t0 += NT) {
+                    const int t2 = t0 + tid;
+                    if (t0 + warp * 32 < nFresh) {
+                        const int sg = t2 < nFresh ? seg_of(fr_i[t2]) : 0;
+                        warp_count(&seg_cnt[sg], sg, 1, t2 < nFresh);
+                    }
+                }
                 __syncthreads();
                 if (warp == 0) { // exclusive scans of counts and min(count, ef)
                     int acc = 0, accf = 0;

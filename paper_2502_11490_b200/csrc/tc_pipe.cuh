@@ -67,47 +67,72 @@ struct TcPipe {
 
     // Score pairs [0, n) (item slot slots[i], query slot gq_of(i)); for every valid row E
     // calls on_score(i, score).  chunk_ctr / tile_ctr: kernel-lifetime counters (all threads).
-    template <class GqOf, class OnScore>
+    template <class OnScore>
     static __device__ __forceinline__ void run(unsigned char *sm, uint32_t tmem, const DevItems &it,
-                                               const DevGraph &g, const int32_t *slots, int n,
-                                               uint32_t &chunk_ctr, uint32_t &tile_ctr, GqOf gq_of,
-                                               OnScore on_score) {
+                                               const DevGraph &g, const int32_t *slots, const int32_t *gis, int n,
+                                               uint32_t &chunk_ctr, uint32_t &tile_ctr,
+                                               OnScore on_score, unsigned long long *sub = nullptr) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+        // role timers (GMPGR_PHASE_TIMING): one writer thread per slot
+        //   0 E layer-0 epilogue  1 E layer-1 epilogue  2 E d0full-wait  3 E d1full-wait  4 E total
+        //   5 issuer full-wait   6 issuer a1full-wait  7 issuer d0empty-wait
+        const long long t_run = sub ? clock64() : 0;
+#define TP_WAIT(slot, expr)                                                   \
+    do {                                                                      \
+        const long long w0_ = sub ? clock64() : 0;                            \
+        expr;                                                                 \
+        if (sub) sub[slot] += (unsigned long long)(clock64() - w0_);          \
+    } while (0)
         const int T = (n + TM - 1) / TM;
         if (T == 0) return;
         if (warp >= L_WARP0) {
             // ================= loaders
             const int lt = tid - 32 * L_WARP0, lw = lt >> 5;
             constexpr int NLW = NL / 32;
-            for (int q = 0; q < T * NC; ++q) {
-                const uint32_t qg = chunk_ctr + q, b = qg & 1u, u = qg >> 1;
-                const int t = q / NC, kc = q % NC, base = t * TM, nv = min(TM, n - base);
-                if (kc == 0 && t + 2 < T) {  // pull tile t+2's rows toward L2 while waiting
-                    constexpr int LPR = D_H / 32;
-                    const int b2 = (t + 2) * TM, n2 = min(TM, n - b2);
-                    for (int j = lt; j < n2 * LPR; j += NL) {
-                        const float *rp = it.emb + slot_row(g, slots[b2 + j / LPR]) * it.ld + (j % LPR) * 32;
-                        asm volatile("prefetch.global.L2 [%0];" ::"l"(rp));
-                    }
+            // Each warp owns units un = lw + NLW*i (8 rows x 4 float4, conflict-free
+            // core-matrix stores).  All of a tile's loads (every K chunk) are issued before the
+            // first empty-wait, so the HBM latency overlaps the tensor core draining the
+            // previous tile instead of being paid once per unit.
+            constexpr int UPC = TM * 16 / 32, UPW = (UPC + NLW - 1) / NLW;
+            for (int t = 0; t < T; ++t) {
+                const int base = t * TM, nv = min(TM, n - base);
+                const float4 *rp[UPW];
+#pragma unroll
+                for (int i = 0; i < UPW; ++i) {
+                    const int un = lw + NLW * i, r = (un % (TM / 8)) * 8 + (lane & 7);
+                    rp[i] = nullptr;
+                    if (un < UPC && r < nv)
+                        rp[i] = reinterpret_cast<const float4 *>(it.emb + slot_row(g, slots[base + r]) * it.ld) +
+                                (un / (TM / 8)) * 4 + (lane >> 3);
                 }
-                if (u >= 1) tc::mbar_wait(bar(sm, EMPTY0 + b), (u - 1) & 1u);
-                unsigned char *Ah = sm + OFF_A + b * 2 * CH_BYTES, *Al = Ah + CH_BYTES;
-                // units of 8 rows x 4 float4 (conflict-free core-matrix stores)
-                for (int un = lw; un < TM * 16 / 32; un += NLW) {
-                    const int r = (un % (TM / 8)) * 8 + (lane & 7), c = (un / (TM / 8)) * 4 + (lane >> 3);
-                    if (r < nv) {
-                        const float4 x = __ldg(reinterpret_cast<const float4 *>(
-                                                   it.emb + slot_row(g, slots[base + r]) * it.ld) + kc * 16 + c);
+                float4 x[NC][UPW];
+#pragma unroll
+                for (int kc = 0; kc < NC; ++kc)
+#pragma unroll
+                    for (int i = 0; i < UPW; ++i)
+                        if (rp[i]) x[kc][i] = __ldg(rp[i] + kc * 16);
+#pragma unroll
+                for (int kc = 0; kc < NC; ++kc) {
+                    const uint32_t qg = chunk_ctr + t * NC + kc, b = qg & 1u, u = qg >> 1;
+                    if (u >= 1) {
+                        tc::mbar_wait(bar(sm, EMPTY0 + b), (u - 1) & 1u);
+                    }
+                    unsigned char *Ah = sm + OFF_A + b * 2 * CH_BYTES, *Al = Ah + CH_BYTES;
+#pragma unroll
+                    for (int i = 0; i < UPW; ++i) {
+                        if (!rp[i]) continue;
+                        const int un = lw + NLW * i, r = (un % (TM / 8)) * 8 + (lane & 7),
+                                  c = (un / (TM / 8)) * 4 + (lane >> 3);
                         uint2 hi, lo;
-                        tc::split4(x, hi, lo);
+                        tc::split4(x[kc][i], hi, lo);
                         const uint32_t off = tc::kmaj_off(r, 4 * c, KC);
                         *reinterpret_cast<uint2 *>(Ah + off) = hi;
                         *reinterpret_cast<uint2 *>(Al + off) = lo;
                     }
+                    tc::fence_async_smem();
+                    asm volatile("bar.sync 14, %0;" ::"r"(NL) : "memory");
+                    if (lt == 0) arrive(bar(sm, FULL0 + b));
                 }
-                tc::fence_async_smem();
-                asm volatile("bar.sync 14, %0;" ::"r"(NL) : "memory");
-                if (lt == 0) arrive(bar(sm, FULL0 + b));
             }
         } else if (warp == ISSUER_WARP) {
             // ================= MMA issuer (one thread)
@@ -117,7 +142,7 @@ struct TcPipe {
                 const uint32_t a1H = tc::smem_u32(sm + OFF_A1H), a1L = tc::smem_u32(sm + OFF_A1L);
                 auto layer1 = [&](int t) {
                     const uint32_t tg = tile_ctr + t;
-                    tc::mbar_wait(bar(sm, A1FULL), tg & 1u);
+                    TP_WAIT(6, tc::mbar_wait(bar(sm, A1FULL), tg & 1u));
                     tc::fence_after();
 #pragma unroll
                     for (int k = 0; k < H / 16; ++k) {
@@ -132,11 +157,11 @@ struct TcPipe {
                 for (int t = 0; t <= T; ++t) {
                     if (t < T) {
                         const uint32_t tg = tile_ctr + t, db = tg & 1u, v = tg >> 1;
-                        if (v >= 1) tc::mbar_wait(bar(sm, D0EMPTY0 + db), (v - 1) & 1u);
+                        if (v >= 1) TP_WAIT(7, tc::mbar_wait(bar(sm, D0EMPTY0 + db), (v - 1) & 1u));
                         const uint32_t d0 = tmem + db * 64;
                         for (int kc = 0; kc < NC; ++kc) {
                             const uint32_t qg = chunk_ctr + t * NC + kc, b = qg & 1u, u = qg >> 1;
-                            tc::mbar_wait(bar(sm, FULL0 + b), u & 1u);
+                            TP_WAIT(5, tc::mbar_wait(bar(sm, FULL0 + b), u & 1u));
                             tc::fence_after();
                             const uint32_t aH = tc::smem_u32(sm + OFF_A + b * 2 * CH_BYTES), aL = aH + CH_BYTES;
 #pragma unroll
@@ -169,10 +194,14 @@ struct TcPipe {
             for (int t = 0; t < T; ++t) {
                 const uint32_t tg = tile_ctr + t, db = tg & 1u, v = tg >> 1;
                 const int base = t * TM, nv = min(TM, n - base);
-                const int gq = row < nv ? gq_of(base + row) : 0;
+                // the row's pair (issued before the wait so the L2 latency hides behind it)
+                const int gi = row < nv ? gis[base + row] : 0, gq = gi >> 16;
+                const int32_t my_s = row < nv ? slots[base + row] : 0;
                 const float *u = Uall + gq * H;
-                tc::mbar_wait(bar(sm, D0FULL0 + db), v & 1u);
+                if (row == 0) TP_WAIT(2, tc::mbar_wait(bar(sm, D0FULL0 + db), v & 1u));
+                else tc::mbar_wait(bar(sm, D0FULL0 + db), v & 1u);
                 tc::fence_after();
+                const long long te0 = (sub && row == 0) ? clock64() : 0;
                 float h[64];
                 {
                     float va[32], vb[32];
@@ -185,8 +214,9 @@ struct TcPipe {
                 arrive(bar(sm, D0EMPTY0 + db));
 #pragma unroll
                 for (int o = 0; o < 64; o += 4) {
-                    float4 y = make_float4(fmaxf(h[o] + u[o], 0.f), fmaxf(h[o + 1] + u[o + 1], 0.f),
-                                           fmaxf(h[o + 2] + u[o + 2], 0.f), fmaxf(h[o + 3] + u[o + 3], 0.f));
+                    const float4 uo = *reinterpret_cast<const float4 *>(u + o);
+                    float4 y = make_float4(fmaxf(h[o] + uo.x, 0.f), fmaxf(h[o + 1] + uo.y, 0.f),
+                                           fmaxf(h[o + 2] + uo.z, 0.f), fmaxf(h[o + 3] + uo.w, 0.f));
                     uint2 hi, lo;
                     tc::split4(y, hi, lo);
                     const uint32_t off = tc::kmaj_off(row, o, H);
@@ -196,8 +226,11 @@ struct TcPipe {
                 tc::fence_async_smem();
                 asm volatile("bar.sync 15, %0;" ::"r"(NE) : "memory");
                 if (row == 0) arrive(bar(sm, A1FULL));
-                tc::mbar_wait(bar(sm, D1FULL), tg & 1u);
+                if (sub && row == 0) sub[0] += (unsigned long long)(clock64() - te0);
+                if (row == 0) TP_WAIT(3, tc::mbar_wait(bar(sm, D1FULL), tg & 1u));
+                else tc::mbar_wait(bar(sm, D1FULL), tg & 1u);
                 tc::fence_after();
+                const long long te1 = (sub && row == 0) ? clock64() : 0;
                 {
                     float va[32], vb[32];
                     tc::tmem_ld32(tmem + lanebase + 128, va);
@@ -206,21 +239,39 @@ struct TcPipe {
                     for (int j = 0; j < 32; ++j) { h[j] = fmaxf(va[j] + b1[j], 0.f); h[32 + j] = fmaxf(vb[j] + b1[32 + j], 0.f); }
                 }
                 tc::fence_before();
+                // approximate path: reassociated (4 partial sums per output) — the exact
+                // refinement re-scores everything near a threshold, so only the error bound matters
                 float s = 0.f;
                 bool bad = false;
+                const float4 *W2v = reinterpret_cast<const float4 *>(W2);
+                float zp[Z][4];
+#pragma unroll
+                for (int o = 0; o < Z; ++o) zp[o][0] = zp[o][1] = zp[o][2] = zp[o][3] = 0.f;
+#pragma unroll
+                for (int j = 0; j < 64; j += 4) {
+#pragma unroll
+                    for (int o = 0; o < Z; ++o) {
+                        const float4 w = W2v[o * (H / 4) + j / 4];
+                        zp[o][0] = fmaf(h[j], w.x, zp[o][0]);
+                        zp[o][1] = fmaf(h[j + 1], w.y, zp[o][1]);
+                        zp[o][2] = fmaf(h[j + 2], w.z, zp[o][2]);
+                        zp[o][3] = fmaf(h[j + 3], w.w, zp[o][3]);
+                    }
+                }
 #pragma unroll
                 for (int o = 0; o < Z; ++o) {
-                    float z = b2[o];
-#pragma unroll
-                    for (int j = 0; j < 64; ++j) z = fmaf(h[j], W2[o * H + j], z);
+                    const float z = b2[o] + ((zp[o][0] + zp[o][1]) + (zp[o][2] + zp[o][3]));
                     bad |= !isfinite(z);
                     s = fmaf(z, att[o], s);
                 }
-                on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s);
+                if (sub && row == 0) sub[1] += (unsigned long long)(clock64() - te1);
+                on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s, gi, my_s);
             }
+            if (sub && row == 0) sub[4] += (unsigned long long)(clock64() - t_run);
         }
         chunk_ctr += T * NC;
         tile_ctr += T;
         __syncthreads();
+#undef TP_WAIT
     }
 };

@@ -88,18 +88,47 @@ __device__ __forceinline__ void tmem_ld32(uint32_t addr, float (&v)[32]) {
     for (int j = 0; j < 32; ++j) v[j] = __uint_as_float(r[j]);
 }
 
+// A operand from tensor memory (".ts" form): lane = row, column c = bf16 pair (k = 2c, 2c+1)
+__device__ __forceinline__ void mma_ts(uint32_t dtmem, uint32_t atmem, uint64_t db, uint32_t id,
+                                       uint32_t acc) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n" ::"r"(dtmem),
+        "r"(atmem), "l"(db), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void tmem_st8(uint32_t addr, const uint32_t (&v)[8]) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(addr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+                 : "memory");
+}
+__device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+// 16-byte global -> shared asynchronous copy (L1 bypass) and the mbarrier arrival that fires
+// when every earlier cp.async of this thread has landed (.noinc: counted in the init count)
+__device__ __forceinline__ void cp_async16(uint32_t sdst, const void *gsrc) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sdst), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
+    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
+    const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+    return *reinterpret_cast<const uint32_t *>(&h);
+}
+
 // split 4 fp32 into bf16 hi/lo pairs packed as 2 x u32 each
 __device__ __forceinline__ void split4(float4 x, uint2 &hi, uint2 &lo) {
-    __nv_bfloat16 h0 = __float2bfloat16_rn(x.x), h1 = __float2bfloat16_rn(x.y),
-                  h2 = __float2bfloat16_rn(x.z), h3 = __float2bfloat16_rn(x.w);
-    __nv_bfloat16 l0 = __float2bfloat16_rn(x.x - __bfloat162float(h0)),
-                  l1 = __float2bfloat16_rn(x.y - __bfloat162float(h1)),
-                  l2 = __float2bfloat16_rn(x.z - __bfloat162float(h2)),
-                  l3 = __float2bfloat16_rn(x.w - __bfloat162float(h3));
-    hi.x = (uint32_t)__bfloat16_as_ushort(h0) | ((uint32_t)__bfloat16_as_ushort(h1) << 16);
-    hi.y = (uint32_t)__bfloat16_as_ushort(h2) | ((uint32_t)__bfloat16_as_ushort(h3) << 16);
-    lo.x = (uint32_t)__bfloat16_as_ushort(l0) | ((uint32_t)__bfloat16_as_ushort(l1) << 16);
-    lo.y = (uint32_t)__bfloat16_as_ushort(l2) | ((uint32_t)__bfloat16_as_ushort(l3) << 16);
+    // hi = bf16(x), lo = bf16(x - hi); cvt.rn.bf16x2.f32 packs two lanes per instruction
+    const __nv_bfloat162 h01 = __floats2bfloat162_rn(x.x, x.y), h23 = __floats2bfloat162_rn(x.z, x.w);
+    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+    const __nv_bfloat162 l01 = __floats2bfloat162_rn(x.x - f01.x, x.y - f01.y),
+                         l23 = __floats2bfloat162_rn(x.z - f23.x, x.w - f23.y);
+    hi.x = *reinterpret_cast<const uint32_t *>(&h01);
+    hi.y = *reinterpret_cast<const uint32_t *>(&h23);
+    lo.x = *reinterpret_cast<const uint32_t *>(&l01);
+    lo.y = *reinterpret_cast<const uint32_t *>(&l23);
 }
 
 } // namespace tc

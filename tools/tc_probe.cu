@@ -41,7 +41,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
          | ((uint32_t)(m >> 4) << 24);
 }
 
-__global__ void probe(const float *A, const float *B, float *D1, float *D3) {
+__global__ void probe(const float *A, const float *B, float *D1, float *D3, float *DT) {
     extern __shared__ __align__(1024) unsigned char sm[];
     // layout: Ahi, Alo (M*K*2 each), Bhi, Blo (N*K*2 each), mbarrier, tmem addr
     unsigned char *sAh = sm, *sAl = sm + M * K * 2, *sBh = sAl + M * K * 2, *sBl = sBh + N * K * 2;
@@ -79,6 +79,27 @@ __global__ void probe(const float *A, const float *B, float *D1, float *D3) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     const uint32_t tmem = *tptr;
     const uint32_t idesc = make_idesc(M, N);
+    // A (bf16 hi) into TMEM cols 192..255 for the TS variant: lane = row, column c holds
+    // the bf16 pair (k = 2c, 2c+1), low half = even k
+    if (warp < 4) {
+        const int row = warp * 32 + lane;
+        for (int c0 = 0; c0 < K / 2; c0 += 8) {
+            uint32_t v[8];
+            for (int j = 0; j < 8; ++j) {
+                const int k = 2 * (c0 + j);
+                __nv_bfloat162 h = __floats2bfloat162_rn(A[row * K + k], A[row * K + k + 1]);
+                v[j] = *reinterpret_cast<uint32_t *>(&h);
+            }
+            const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + 192 + c0;
+            asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};"
+                         :: "r"(addr), "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]),
+                            "r"(v[6]), "r"(v[7]) : "memory");
+        }
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
     if (tid == 0) {
         // pass 1: D[cols 0..63] = Ahi . Bhi ; pass 2: D[cols 64..127] = hi.hi + hi.lo + lo.hi
         for (int pass = 0; pass < 2; ++pass) {
@@ -99,6 +120,14 @@ __global__ void probe(const float *A, const float *B, float *D1, float *D3) {
                 }
             }
         }
+        // pass 3 (TS): D[cols 128..191] = A(TMEM) . Bhi
+        for (int kk = 0; kk < K / 16; ++kk) {
+            uint64_t db = make_desc(smem_u32(sBh) + kk * 256, 128, K * 16);
+            asm volatile(
+                "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}\n"
+                :: "r"(tmem + 128), "r"(tmem + 192 + kk * 8), "l"(db), "r"(idesc), "r"((uint32_t)(kk > 0)));
+        }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];"
                      :: "r"(smem_u32(bar)) : "memory");
     }
@@ -113,7 +142,7 @@ __global__ void probe(const float *A, const float *B, float *D1, float *D3) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     if (warp < 4) {
         const int row = warp * 32 + lane;
-        for (int pass = 0; pass < 2; ++pass) {
+        for (int pass = 0; pass < 3; ++pass) {
             for (int c0 = 0; c0 < N; c0 += 8) {
                 uint32_t v[8];
                 const uint32_t addr = tmem + ((uint32_t)(warp * 32) << 16) + pass * 64 + c0;
@@ -121,14 +150,14 @@ __global__ void probe(const float *A, const float *B, float *D1, float *D3) {
                              : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
                                "=r"(v[6]), "=r"(v[7]) : "r"(addr));
                 asm volatile("tcgen05.wait::ld.sync.aligned;");
-                float *D = pass == 0 ? D1 : D3;
+                float *D = pass == 0 ? D1 : pass == 1 ? D3 : DT;
                 for (int j = 0; j < 8; ++j) D[row * N + c0 + j] = __uint_as_float(v[j]);
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;");
     __syncthreads();
-    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(128));
+    if (warp == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" :: "r"(tmem), "r"(256));
 }
 
 static float bf(float x) { // round-to-nearest-even to bf16, back to float
@@ -144,19 +173,25 @@ int main() {
     srand(1);
     for (int i = 0; i < M * K; ++i) hA[i] = (rand() / (float)RAND_MAX - 0.5f) * 4.f;
     for (int i = 0; i < N * K; ++i) hB[i] = (rand() / (float)RAND_MAX - 0.5f) * 0.3f;
-    float *dA, *dB, *dD1, *dD3;
+    float *dA, *dB, *dD1, *dD3, *dDT;
+    CK(cudaMalloc(&dDT, M * N * 4));
     CK(cudaMalloc(&dA, M * K * 4)); CK(cudaMalloc(&dB, N * K * 4));
     CK(cudaMalloc(&dD1, M * N * 4)); CK(cudaMalloc(&dD3, M * N * 4));
     CK(cudaMemcpy(dA, hA, M * K * 4, cudaMemcpyHostToDevice));
     CK(cudaMemcpy(dB, hB, N * K * 4, cudaMemcpyHostToDevice));
     int smem = 2 * M * K * 2 + 2 * N * K * 2 + 64;
     CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    probe<<<1, 256, smem>>>(dA, dB, dD1, dD3);
+    probe<<<1, 256, smem>>>(dA, dB, dD1, dD3, dDT);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     float *D1 = (float *)malloc(M * N * 4), *D3 = (float *)malloc(M * N * 4);
     CK(cudaMemcpy(D1, dD1, M * N * 4, cudaMemcpyDeviceToHost));
     CK(cudaMemcpy(D3, dD3, M * N * 4, cudaMemcpyDeviceToHost));
+    float *DT = (float *)malloc(M * N * 4);
+    CK(cudaMemcpy(DT, dDT, M * N * 4, cudaMemcpyDeviceToHost));
+    int ts_bad = 0;
+    for (int i = 0; i < M * N; ++i) ts_bad += DT[i] != D1[i];
+    printf("TS (A in TMEM) vs SS bf16: %d / %d differ\n", ts_bad, M * N);
     double e1 = 0, e3 = 0, e3rel = 0;
     for (int r = 0; r < M; ++r)
         for (int c = 0; c < N; ++c) {
@@ -172,7 +207,7 @@ int main() {
         }
     printf("bf16 MMA vs fp64 of bf16 inputs: max err / sum|ab| = %.3e\n", e1);
     printf("bf16x3 vs fp64 of fp32 inputs:    max err / sum|ab| = %.3e (rel %.3e)\n", e3, e3rel);
-    printf("%s\n", (e1 < 1e-5 && e3 < 1e-4) ? "PROBE OK" : "PROBE MISMATCH");
+    printf("%s\n", (e1 < 1e-5 && e3 < 1e-4 && ts_bad == 0) ? "PROBE OK" : "PROBE MISMATCH");
     printf("D1[0..3] = %f %f %f %f\n", D1[0], D1[1], D1[2], D1[3]);
     return 0;
 }
