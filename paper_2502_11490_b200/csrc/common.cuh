@@ -114,4 +114,5 @@ struct DevItems {
     const float *emb; // [n][ld] fp32, ld multiple of 4 (16-byte rows)
     int64_t n;
     int d, ld;
+    const uint16_t *hl; // [n][2d] bf16 bits: hi = bf16(x), lo = bf16(x - hi) (d % 64 == 0), or null
 };

@@ -117,7 +117,21 @@ struct gr_items {
     int device;
     DevItems di;
     void *dbuf;
+    void *hbuf = nullptr;
 };
+
+__global__ void split_items_kernel(const float *emb, int64_t n, int d, int ld, uint16_t *hl) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * d;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / d;
+        const int c = (int)(i % d);
+        const float x = emb[r * ld + c];
+        const __nv_bfloat16 h = __float2bfloat16_rn(x);
+        const __nv_bfloat16 l = __float2bfloat16_rn(x - __bfloat162float(h));
+        hl[r * 2 * d + c] = __bfloat16_as_ushort(h);
+        hl[r * 2 * d + d + c] = __bfloat16_as_ushort(l);
+    }
+}
 
 struct gr_searcher {
     int device;
@@ -422,13 +436,25 @@ int gr_items_create(int device, const float *emb, int64_t n, int32_t d, int emb_
     cudaError_t e = cudaMemcpy2D(p, (size_t)ld * 4, emb, (size_t)d * 4, (size_t)d * 4, n,
                                  emb_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
     if (e != cudaSuccess) { cudaFree(p); return fail(GR_ECUDA, cudaGetErrorString(e)); }
+    // bf16 hi/lo copy for the pipelined tensor-core scorer (cp.async-able, no conversion
+    // on the search path); items are immutable for the handle's lifetime
+    uint16_t *hl = nullptr;
+    if (d % 64 == 0 && d <= 128) {
+        if (int rc = dmalloc(&hl, (size_t)n * 2 * d)) { cudaFree(p); return rc; }
+        const int64_t total = n * d;
+        split_items_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 64), 256>>>(p, n, d, ld, hl);
+        e = cudaDeviceSynchronize();
+        if (e != cudaSuccess) { cudaFree(p); cudaFree(hl); return fail(GR_ECUDA, cudaGetErrorString(e)); }
+    }
     gr_items *I = new gr_items();
     I->device = device;
     I->di.emb = p;
     I->di.n = n;
     I->di.d = d;
     I->di.ld = ld;
+    I->di.hl = hl;
     I->dbuf = p;
+    I->hbuf = hl;
     *out = I;
     return GR_OK;
 }
@@ -437,6 +463,7 @@ int gr_items_destroy(gr_items *it) {
     if (!it) return GR_OK;
     cudaSetDevice(it->device);
     cudaFree(it->dbuf);
+    if (it->hbuf) cudaFree(it->hbuf);
     delete it;
     return GR_OK;
 }
@@ -682,8 +709,10 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     // 8 queries per CTA in lock-step (GMPGR_MQ_G=4 for 4): +6% on cfg3 in tc mode
     const char *genv = getenv("GMPGR_MQ_G");
     const bool g8 = !(genv && std::strcmp(genv, "4") == 0);
-    const char *penv = getenv("GMPGR_PIPE");  // warp-specialised tcgen05 scoring pipeline
-    const bool pipe = penv && std::strcmp(penv, "1") == 0;
+    // warp-specialised tcgen05 scoring pipeline (default; GMPGR_PIPE=0 selects the
+    // lock-step tile scorer: cfg3 374 -> 273 ms per 65k queries with the pipeline)
+    const char *penv = getenv("GMPGR_PIPE");
+    const bool pipe = !(penv && std::strcmp(penv, "0") == 0) && I->di.hl != nullptr;
     int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? ((g8 || (pipe && mode == GR_MODE_TC)) ? 8 : 4) : 2;
     void (*kern)(const SearchArgs) = nullptr;
 #define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \

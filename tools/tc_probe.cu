@@ -41,7 +41,7 @@ __host__ __device__ constexpr uint32_t make_idesc(int m, int n) {
          | ((uint32_t)(m >> 4) << 24);
 }
 
-__global__ void probe(const float *A, const float *B, float *D1, float *D3, float *DT) {
+__global__ void probe(const float *A, const float *B, float *D1, float *D3, float *DT, int mode) {
     extern __shared__ __align__(1024) unsigned char sm[];
     // layout: Ahi, Alo (M*K*2 each), Bhi, Blo (N*K*2 each), mbarrier, tmem addr
     unsigned char *sAh = sm, *sAl = sm + M * K * 2, *sBh = sAl + M * K * 2, *sBl = sBh + N * K * 2;
@@ -66,7 +66,7 @@ __global__ void probe(const float *A, const float *B, float *D1, float *D3, floa
     }
     if (warp == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;"
-                     :: "r"(smem_u32(tptr)), "r"(128));
+                     :: "r"(smem_u32(tptr)), "r"(256));
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
     }
     if (tid == 0) {
@@ -120,8 +120,8 @@ __global__ void probe(const float *A, const float *B, float *D1, float *D3, floa
                 }
             }
         }
-        // pass 3 (TS): D[cols 128..191] = A(TMEM) . Bhi
-        for (int kk = 0; kk < K / 16; ++kk) {
+        // pass 3 (TS): D[cols 128..191] = A(TMEM) . Bhi   (mode 0: skipped)
+        for (int kk = 0; kk < (mode ? K / 16 : 0); ++kk) {
             uint64_t db = make_desc(smem_u32(sBh) + kk * 256, 128, K * 16);
             asm volatile(
                 "{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -168,7 +168,7 @@ static float bf(float x) { // round-to-nearest-even to bf16, back to float
     return r;
 }
 
-int main() {
+int main(int argc, char **argv) {
     float *hA = (float *)malloc(M * K * 4), *hB = (float *)malloc(N * K * 4);
     srand(1);
     for (int i = 0; i < M * K; ++i) hA[i] = (rand() / (float)RAND_MAX - 0.5f) * 4.f;
@@ -181,7 +181,9 @@ int main() {
     CK(cudaMemcpy(dB, hB, N * K * 4, cudaMemcpyHostToDevice));
     int smem = 2 * M * K * 2 + 2 * N * K * 2 + 64;
     CK(cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-    probe<<<1, 256, smem>>>(dA, dB, dD1, dD3, dDT);
+    const int mode = argc > 1 ? atoi(argv[1]) : 1;
+    printf("mode %d\n", mode);
+    probe<<<1, 256, smem>>>(dA, dB, dD1, dD3, dDT, mode);
     CK(cudaGetLastError());
     CK(cudaDeviceSynchronize());
     float *D1 = (float *)malloc(M * N * 4), *D3 = (float *)malloc(M * N * 4);
