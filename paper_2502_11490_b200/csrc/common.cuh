@@ -115,4 +115,5 @@ struct DevItems {
     int64_t n;
     int d, ld;
     const uint16_t *hl; // [n][2d] bf16 bits: hi = bf16(x), lo = bf16(x - hi) (d % 64 == 0), or null
+    int hl_by_slot;     // hl rows indexed by graph slot (graph-owned copy) instead of item row
 };

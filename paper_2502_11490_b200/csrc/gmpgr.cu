@@ -5,9 +5,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <mutex>
 #include <numeric>
 #include <string>
 #include <vector>
@@ -111,6 +113,11 @@ struct gr_graph {
     DevGraph dg;
     std::vector<void *> bufs;
     int max_deg;
+    // bf16 hi/lo item rows in device-slot order for one items handle (built on first use),
+    // so the scorer's gathers follow the graph's locality and need no row indirection
+    std::mutex hl_mu;
+    uint64_t hl_serial = 0;
+    uint16_t *hl_slot = nullptr;
 };
 
 struct gr_items {
@@ -118,7 +125,22 @@ struct gr_items {
     DevItems di;
     void *dbuf;
     void *hbuf = nullptr;
+    uint64_t serial = 0;
 };
+static std::atomic<uint64_t> g_items_serial{0};
+
+__global__ void gather_hl_kernel(const uint16_t *hl, const int32_t *rows, int64_t n, int d,
+                                 uint16_t *out) {
+    // one 16-byte piece per thread: row s of out = row rows[s] of hl ([n][2d] bf16)
+    const int per = 2 * d / 8;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * per;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t s = i / per;
+        const int c = (int)(i % per);
+        reinterpret_cast<uint4 *>(out + s * 2 * d)[c] =
+            reinterpret_cast<const uint4 *>(hl + (int64_t)rows[s] * 2 * d)[c];
+    }
+}
 
 __global__ void split_items_kernel(const float *emb, int64_t n, int d, int ld, uint16_t *hl) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n * d;
@@ -316,37 +338,79 @@ int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *n
         delete G;
         return rc;
     };
+    for (int l = 0; l < n_layers; ++l)
+        if (row_stride[l] < 0 || row_stride[l] > 4096) return cleanup(fail(GR_EINVAL, "row stride out of range"));
+    // Device slot order: breadth-first from the entry over layer 0 (GMPGR_REORDER=0 keeps the
+    // caller's order).  Graph neighbours get nearby device slots, so the per-query visited
+    // tags and adjacency rows they touch share L2 lines.  Invisible to callers: results are
+    // reported by id and every tie-break uses the id rank, never the slot.
+    std::vector<int64_t> perm;  // device slot -> caller slot (empty = identity)
+    std::vector<int32_t> inv;   // caller slot -> device slot
+    {
+        const char *renv = getenv("GMPGR_REORDER");
+        if (!(renv && std::strcmp(renv, "0") == 0) && n > 1) {
+            perm.reserve(n);
+            inv.assign(n, -1);
+            const int64_t st0 = row_stride[0];
+            auto visit_from = [&](int64_t root) {
+                size_t head = perm.size();
+                inv[root] = (int32_t)perm.size();
+                perm.push_back(root);
+                while (head < perm.size()) {
+                    const int64_t o = perm[head++];
+                    const int32_t c = cnts[0][o];
+                    if (c <= 0 || c > st0) continue;
+                    const int32_t *src = nbrs[0] + o * st0;
+                    for (int j = 0; j < c; ++j) {
+                        const int32_t v = src[j];
+                        if (v >= 0 && v < n && inv[v] < 0) {
+                            inv[v] = (int32_t)perm.size();
+                            perm.push_back(v);
+                        }
+                    }
+                }
+            };
+            visit_from(entry_slot);
+            for (int64_t o = 0; o < n; ++o)
+                if (inv[o] < 0) visit_from(o);
+        }
+    }
+    const bool re = !perm.empty();
+    auto old_of = [&](int64_t s) { return re ? perm[s] : s; };
+    auto new_of = [&](int32_t o) { return re ? inv[o] : o; };
+    dg.entry = new_of(entry_slot);
     // upper-layer membership: level >= 1 (index.py:77, nesting); fall back to "has edges"
     std::vector<int32_t> up_row(n, -1);
     int64_t n_up = 0;
     if (n_layers > 1) {
         for (int64_t s = 0; s < n; ++s) {
-            bool member = levels ? levels[s] >= 1 : false;
+            const int64_t o = old_of(s);
+            bool member = levels ? levels[o] >= 1 : false;
             if (!levels)
-                for (int l = 1; l < n_layers; ++l) member |= cnts[l][s] > 0;
+                for (int l = 1; l < n_layers; ++l) member |= cnts[l][o] > 0;
             if (member) up_row[s] = (int32_t)n_up++;
         }
     }
     for (int l = 0; l < n_layers; ++l) {
         const int64_t stride = row_stride[l];
-        if (stride < 0 || stride > 4096) return cleanup(fail(GR_EINVAL, "row stride out of range"));
         const int deg = (int)std::max<int64_t>(stride, 1);
         const int ld = round4(deg);
         const int64_t nrows = l == 0 ? n : std::max<int64_t>(n_up, 1);
         std::vector<int32_t> h((size_t)nrows * ld, -1);
         for (int64_t s = 0; s < n; ++s) {
-            const int32_t c = cnts[l][s];
+            const int64_t o = old_of(s);
+            const int32_t c = cnts[l][o];
             if (c == 0) continue;
             if (c < 0 || c > stride)
                 return cleanup(fail(GR_EINVAL, "layer " + std::to_string(l) + " slot " +
-                                                   std::to_string(s) + ": bad neighbour count"));
+                                                   std::to_string(o) + ": bad neighbour count"));
             int64_t r = l == 0 ? s : up_row[s];
             if (r < 0) continue; // not a member of this layer: never expanded
-            const int32_t *src = nbrs[l] + s * stride;
+            const int32_t *src = nbrs[l] + o * stride;
             for (int j = 0; j < c; ++j) {
                 if (src[j] < 0 || src[j] >= n)
                     return cleanup(fail(GR_EINVAL, "neighbour slot out of range"));
-                h[(size_t)r * ld + j] = src[j];
+                h[(size_t)r * ld + j] = new_of(src[j]);
             }
         }
         int32_t *d = nullptr;
@@ -370,7 +434,13 @@ int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *n
         int64_t *d = nullptr;
         if (int rc = dmalloc(&d, n)) return cleanup(rc);
         G->bufs.push_back(d);
-        cudaMemcpy(d, ids, n * 8, cudaMemcpyHostToDevice);
+        if (re) {
+            std::vector<int64_t> ids_dev(n);
+            for (int64_t s = 0; s < n; ++s) ids_dev[s] = ids[perm[s]];
+            cudaMemcpy(d, ids_dev.data(), n * 8, cudaMemcpyHostToDevice);
+        } else {
+            cudaMemcpy(d, ids, n * 8, cudaMemcpyHostToDevice);
+        }
         dg.ids = d;
     }
     // embedding rows: explicit, else ids (model_scorer convention); identity -> nullptr
@@ -378,7 +448,8 @@ int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *n
         std::vector<int32_t> r(n);
         bool ident = true;
         for (int64_t s = 0; s < n; ++s) {
-            const int64_t v = rows ? (int64_t)rows[s] : ids[s];
+            const int64_t o = old_of(s);
+            const int64_t v = rows ? (int64_t)rows[o] : ids[o];
             if (v < 0 || v > 0x7fffffffLL)
                 return cleanup(fail(GR_EINVAL, "item ids must be row indexes >= 0 (search.py:84-90)"));
             r[s] = (int32_t)v;
@@ -394,13 +465,17 @@ int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *n
     }
     // tie-break rank: slot when ids ascend, else rank of id
     {
+        auto id_of = [&](int64_t s) { return ids[old_of(s)]; };
         bool mono = true;
-        for (int64_t s = 1; s < n && mono; ++s) mono = ids[s] > ids[s - 1];
+        for (int64_t s = 1; s < n && mono; ++s) mono = id_of(s) > id_of(s - 1);
         if (!mono) {
             std::vector<int64_t> order(n);
             std::iota(order.begin(), order.end(), 0);
             std::stable_sort(order.begin(), order.end(),
-                             [&](int64_t a, int64_t b) { return ids[a] < ids[b]; });
+                             [&](int64_t a, int64_t b) {
+                                 const int64_t ia = id_of(a), ib = id_of(b);
+                                 return ia < ib || (ia == ib && old_of(a) < old_of(b));
+                             });
             std::vector<uint32_t> rank(n);
             for (int64_t i = 0; i < n; ++i) rank[order[i]] = (uint32_t)i;
             uint32_t *d = nullptr;
@@ -419,6 +494,7 @@ int gr_graph_destroy(gr_graph *g) {
     if (!g) return GR_OK;
     cudaSetDevice(g->device);
     for (void *p : g->bufs) cudaFree(p);
+    if (g->hl_slot) cudaFree(g->hl_slot);
     delete g;
     return GR_OK;
 }
@@ -455,6 +531,7 @@ int gr_items_create(int device, const float *emb, int64_t n, int32_t d, int emb_
     I->di.hl = hl;
     I->dbuf = p;
     I->hbuf = hl;
+    I->serial = ++g_items_serial;
     *out = I;
     return GR_OK;
 }
@@ -695,6 +772,21 @@ int plan_mq(int k, int kp, SearchArgs &a) {
     return P.bytes;
 }
 
+int ensure_slot_hl(gr_graph *G, const gr_items *I, cudaStream_t stream) {
+    std::lock_guard<std::mutex> lk(G->hl_mu);
+    if (G->hl_slot && G->hl_serial == I->serial) return GR_OK;
+    if (I->di.n < G->dg.n) return fail(GR_EINVAL, "items table smaller than the graph");
+    if (!G->hl_slot) {
+        if (int rc = dmalloc(&G->hl_slot, (size_t)G->dg.n * 2 * I->di.d)) return rc;
+    }
+    const int64_t work = G->dg.n * (2 * I->di.d / 8);
+    gather_hl_kernel<<<(unsigned)std::min<int64_t>((work + 255) / 256, 148 * 64), 256, 0, stream>>>(
+        I->di.hl, G->dg.rows, G->dg.n, I->di.d, G->hl_slot);
+    GR_CUDA(cudaGetLastError());
+    G->hl_serial = I->serial;
+    return GR_OK;
+}
+
 // multi-query kernel for the fixed model shapes (search_mq.cuh); returns -1 if not applicable
 int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I,
               const float *users, int64_t Q, const gr_search_params *p, int64_t *ids,
@@ -760,6 +852,11 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     a.g = G->dg;
     a.M = M->dm;
     a.it = I->di;
+    if (pipe && mode == GR_MODE_TC && G->dg.rows) {
+        if (int rc = ensure_slot_hl(const_cast<gr_graph *>(G), I, stream)) return rc;
+        a.it.hl = G->hl_slot;
+        a.it.hl_by_slot = 1;
+    }
     a.users = users;
     a.Q = Q;
     a.k = p->k;

@@ -111,7 +111,9 @@ struct TcPipe {
                 const uint16_t *rp[UPW];
 #pragma unroll
                 for (int i = 0; i < UPW; ++i)
-                    rp[i] = nxt[i] >= 0 ? it.hl + slot_row(g, nxt[i]) * (2 * (int64_t)D_H) : nullptr;
+                    rp[i] = nxt[i] >= 0 ? it.hl + (it.hl_by_slot ? (int64_t)nxt[i] : slot_row(g, nxt[i])) *
+                                                      (2 * (int64_t)D_H)
+                                        : nullptr;
                 if (t + 1 < T) load_slots(t + 1);
 #pragma unroll
                 for (int kc = 0; kc < NC; ++kc) {
