@@ -20,6 +20,9 @@
  *                        (search.py:194-286, 30-70), batched over Q user embeddings
  *   gr_brute_force    <- brute_force(model_scorer(...), ids, k) (search.py:93-108)
  *   gr_merge_topk     <- CandidatePool(k).push(...) over several result lists (pool.py:11-55)
+ *   gr_scores_euclid  <- euclidean_scorer(query, item_vectors) (search.py:73-81), Q queries
+ *   gr_scores_create  <- an arbitrary ScoreFn (search.py:27) tabulated as fp64 [Q, n_items]
+ *   gr_search_scores  <- c_hipanns(index, <that ScoreFn>, SearchParams) (search.py:194-286)
  *
  * Pointer arguments documented "host-or-device" follow the `on_device` flag of
  * the call: 0 = host memory (the library copies in/out on `stream` and
@@ -49,6 +52,7 @@ typedef struct gr_model gr_model;
 typedef struct gr_graph gr_graph;
 typedef struct gr_items gr_items;
 typedef struct gr_searcher gr_searcher;
+typedef struct gr_scores gr_scores;
 
 /* Search knobs = SearchParams (search.py:30-49); ef is frontier_width (ef or 2k).
  * mode: GR_MODE_EXACT (every claim scored by the exact-fp32 CUDA-core scorer) or
@@ -157,6 +161,28 @@ int gr_brute_force(const gr_model *m, const gr_items *it, const float *users, in
 int gr_merge_topk(int device, const int64_t *in_ids, const double *in_scores, int32_t R,
                   int64_t Q, int32_t k_in, int32_t k, int64_t *out_ids, double *out_scores,
                   int32_t *out_count, void *stream);
+
+/* Traversal-only scorers (the reference's search tests: search.py:73-81 euclidean_scorer and
+ * ad-hoc ScoreFns).  A score table holds fp64 scores [Q, n_items] indexed by ITEM ID (ids are
+ * score-table columns, like euclidean_scorer's `item_vectors[ids]`, search.py:79).
+ * gr_scores_create: host-or-device fp64 table.  GR_ENUMERIC if any score is NaN.
+ * gr_scores_euclid: host fp64 vectors [n_items, dim] and queries [Q, dim]; computes
+ *   -sqrt(einsum('ij,ij->i', v - q, v - q)) on the device in numpy's fp64 order (bit-exact).
+ * gr_scores_read: copy the fp64 table to host memory [Q, n_items]. */
+int gr_scores_create(int device, const double *table, int64_t Q, int64_t n_items, int on_device,
+                     gr_scores **out);
+int gr_scores_euclid(int device, const double *vectors, int64_t n_items, int32_t dim,
+                     const double *queries, int64_t Q, gr_scores **out);
+int gr_scores_read(const gr_scores *t, double *out);
+int gr_scores_destroy(gr_scores *t);
+
+/* Batched C-HiPANNS driven by a score table (query q of the batch = row q of the table):
+ * same semantics, outputs and stats as gr_search (exact mode only); returned scores are the
+ * table's fp64 values.  Every graph item id must be < n_items (GR_EINVAL otherwise).
+ * host-or-device output pointers; synchronous for host outputs. */
+int gr_search_scores(gr_searcher *s, const gr_graph *g, const gr_scores *t,
+                     const gr_search_params *p, int64_t *out_ids, double *out_scores,
+                     int32_t *out_count, int64_t *out_stats, int on_device, void *stream);
 
 #ifdef __cplusplus
 }

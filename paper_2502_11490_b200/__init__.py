@@ -39,9 +39,12 @@ from .search import (
     brute_force_batch,
     c_hipanns,
     c_hipanns_batch,
+    c_hipanns_scores_batch,
     coverage,
+    euclidean_scorer,
     model_scorer,
     recall_at,
+    table_scorer,
 )
 
 __version__ = "0.1.0"
@@ -51,6 +54,7 @@ __all__ = [
     "GpuBatchEngine", "GraphIndex", "InvalidArgumentError", "MetricModel", "NannError",
     "NumericError", "Projector", "QueueShutdownError", "RelevanceModel", "SearchParams",
     "SearchResult", "SearchStats", "WeightOverflowError", "brute_force", "brute_force_batch",
-    "c_hipanns", "c_hipanns_batch", "coverage", "create_model", "load_model", "model_scorer",
+    "c_hipanns", "c_hipanns_batch", "c_hipanns_scores_batch", "coverage", "euclidean_scorer",
+    "table_scorer", "create_model", "load_model", "model_scorer",
     "project", "quantize", "recall_at", "relevance", "relevance_batch", "save_model",
 ]

@@ -30,6 +30,8 @@ EXPORTS = (
     "gr_search", "gr_search_async", "gr_searcher_status", "gr_searcher_launches",
     "gr_searcher_counters",
     "gr_brute_force", "gr_merge_topk",
+    "gr_scores_create", "gr_scores_euclid", "gr_scores_read", "gr_scores_destroy",
+    "gr_search_scores",
 )
 
 
@@ -70,6 +72,11 @@ def _declare(lib):
         "gr_searcher_counters": (C.c_int, [vp, vp]),
         "gr_brute_force": (C.c_int, [vp, vp, vp, i64, i32, vp, vp, C.c_int, vp]),
         "gr_merge_topk": (C.c_int, [C.c_int, vp, vp, i32, i64, i32, i32, vp, vp, vp, vp]),
+        "gr_scores_create": (C.c_int, [C.c_int, vp, i64, i64, C.c_int, vp]),
+        "gr_scores_euclid": (C.c_int, [C.c_int, vp, i64, i32, vp, i64, vp]),
+        "gr_scores_read": (C.c_int, [vp, vp]),
+        "gr_scores_destroy": (C.c_int, [vp]),
+        "gr_search_scores": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)
@@ -217,6 +224,34 @@ class DeviceItems(_Handle):
         super().__init__(h, device)
 
 
+class DeviceScores(_Handle):
+    """gr_scores: traversal-only fp64 score table [Q, n_items] by item id (test scorers)."""
+    _destroy = "gr_scores_destroy"
+
+    def __init__(self, table=None, *, vectors=None, queries=None, device: int | None = None):
+        require_device()
+        device = current_device() if device is None else device
+        h = C.c_void_p()
+        if table is not None:
+            table = np.ascontiguousarray(np.atleast_2d(table), dtype=np.float64)
+            self.Q, self.n = table.shape
+            check(lib().gr_scores_create(device, ptr(table), self.Q, self.n, 0, C.byref(h)))
+        else:
+            vectors = np.ascontiguousarray(vectors, dtype=np.float64)
+            if vectors.ndim == 1:
+                vectors = vectors[:, None]
+            queries = np.ascontiguousarray(queries, dtype=np.float64).reshape(-1, vectors.shape[1])
+            self.Q, self.n = queries.shape[0], vectors.shape[0]
+            check(lib().gr_scores_euclid(device, ptr(vectors), self.n, vectors.shape[1],
+                                         ptr(queries), self.Q, C.byref(h)))
+        super().__init__(h, device)
+
+    def read(self) -> np.ndarray:
+        out = np.empty((self.Q, self.n), dtype=np.float64)
+        check(lib().gr_scores_read(self.h, ptr(out)))
+        return out
+
+
 class DeviceSearcher(_Handle):
     """gr_searcher: per-stream scratch for gr_search."""
     _destroy = "gr_searcher_destroy"
@@ -240,7 +275,7 @@ class DeviceSearcher(_Handle):
             names = ("init", "seeds", "expand", "resolve", "score", "pool", "frontier", "output")
             tot = float(out[2:10].sum())
             d["phase_share"] = {k: round(float(v) / tot, 4) for k, v in zip(names, out[2:10])}
-            if os.environ.get("GMPGR_PIPE", "1") != "0" and out[10:18].any():
+            if out[10:18].any():
                 sub = ("e_epi0", "e_epi1", "e_d0full_wait", "e_d1full_wait", "e_total",
                        "is_full_wait", "is_a1full_wait", "ld_empty_wait")
                 d["pipe_share"] = {k: round(float(v) / tot, 4) for k, v in zip(sub, out[10:18])}

@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "search_kernel.cuh"
 #include "search_mq.cuh"
+#include "scores.cuh"
 
 namespace {
 
@@ -154,6 +155,13 @@ __global__ void split_items_kernel(const float *emb, int64_t n, int d, int ld, u
         hl[r * 2 * d + d + c] = __bfloat16_as_ushort(l);
     }
 }
+
+struct gr_scores {
+    int device;
+    int64_t Q = 0, n = 0;
+    double *tab = nullptr;   // [Q][n] fp64 scores by item id
+    uint32_t *code = nullptr; // [Q][n] per-query dense rank + 1 (scores.cuh)
+};
 
 struct gr_searcher {
     int device;
@@ -794,39 +802,24 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
     const int mode = p->mode;
-    // one 512-thread CTA per SM, 4 queries (GMPGR_MQ=256: two 256-thread CTAs, 2 queries
-    // each, tensor-core mode only -- measured slower on cfg3: 854 vs 590 ms per 65k queries)
-    const char *menv = getenv("GMPGR_MQ");
-    const bool wide = mode != GR_MODE_TC || !(menv && std::strcmp(menv, "256") == 0);
-    // 8 queries per CTA in lock-step (GMPGR_MQ_G=4 for 4): +6% on cfg3 in tc mode
-    const char *genv = getenv("GMPGR_MQ_G");
-    const bool g8 = !(genv && std::strcmp(genv, "4") == 0);
-    // warp-specialised tcgen05 scoring pipeline (default; GMPGR_PIPE=0 selects the
-    // lock-step tile scorer: cfg3 374 -> 273 ms per 65k queries with the pipeline)
-    const char *penv = getenv("GMPGR_PIPE");
-    const bool pipe = !(penv && std::strcmp(penv, "0") == 0) && I->di.hl != nullptr;
-    int smem = 0, nthreads = wide ? 512 : 256, gq = wide ? ((g8 || (pipe && mode == GR_MODE_TC)) ? 8 : 4) : 2;
+    // One 512-thread CTA per SM, 8 queries in lock-step.  Tensor-core mode runs the
+    // warp-specialised tcgen05 scoring pipeline (tc_pipe.cuh) and needs the bf16 hi/lo item
+    // copy; without it the per-query kernel (search_kernel.cuh) runs.  Measured on cfg3
+    // (65,536 queries, tc): 2x256-thread CTAs x 2 queries 854 ms, 1x512 x 4 queries 590 ms,
+    // 8 queries +6%, lock-step tile scorer 374 ms -> pipelined scorer 273 ms -> + BFS slot
+    // order 237 ms (those variants were retired from the build).
+    if (mode == GR_MODE_TC && I->di.hl == nullptr) return -1;
+    const bool pipe = mode == GR_MODE_TC;
+    int smem = 0, nthreads = 512, gq = 8;
     void (*kern)(const SearchArgs) = nullptr;
 #define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \
     case CODE:                                                                                     \
-        if (mode == GR_MODE_TC && wide && pipe) {                                                  \
+        if (pipe) {                                                                                \
             smem = plan_mq<DH, ZZ, 1, 512, 8, DH, true>(p->k, p->k_parallel, a);                   \
             kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH, true>;                                 \
-        } else if (mode == GR_MODE_TC && wide && g8) {                                             \
-            smem = plan_mq<DH, ZZ, 1, 512, 8, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH, false>;                                       \
-        } else if (mode == GR_MODE_TC && wide) {                                                   \
-            smem = plan_mq<DH, ZZ, 1, 512, 4, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 4, DH, false>;                                       \
-        } else if (mode == GR_MODE_TC) {                                                           \
-            smem = plan_mq<DH, ZZ, 1, 256, 2, 64>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 256, 2, 64, false>;                                       \
-        } else if (g8) {                                                                           \
-            smem = plan_mq<DH, ZZ, 0, 512, 8, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH, false>;                                       \
         } else {                                                                                   \
-            smem = plan_mq<DH, ZZ, 0, 512, 4, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 4, DH, false>;                                       \
+            smem = plan_mq<DH, ZZ, 0, 512, 8, DH>(p->k, p->k_parallel, a);                         \
+            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH, false>;                                \
         }                                                                                          \
         break;
     switch (shape) {
@@ -1038,7 +1031,74 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     return GR_OK;
 }
 
+// traversal-only score-table search (MODE 2 of hipanns_search_kernel, scores.cuh)
+int launch_search_scores(gr_searcher *S, const gr_graph *G, const gr_scores *T,
+                         const gr_search_params *p, int64_t *ids, double *scores, int32_t *count,
+                         int64_t *stats, cudaStream_t stream) {
+    SearchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    SmemPlan P;
+    a.off_hist = P.alloc(GR_NW * 256 * 4);
+    a.sortcap = pow2ceil(std::max(p->k, p->k_parallel));
+    a.off_sortk = P.alloc(a.sortcap * 8);
+    a.off_sortv = P.alloc(a.sortcap * 4);
+    a.off_kp = P.alloc(3 * p->k_parallel * 4);
+    const int smem = P.bytes;
+    auto kern = smem <= 110 * 1024 ? hipanns_search_kernel<2, 0, 0, 2> : hipanns_search_kernel<1, 0, 0, 2>;
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 0;
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GR_NT, smem));
+    if (per_sm < 1) return fail(GR_EINVAL, "search kernel does not fit on an SM");
+    const int64_t Q = T->Q;
+    int64_t slots = std::min<int64_t>(Q, (int64_t)per_sm * num_sms(G->device));
+    const int64_t capF = (int64_t)p->k_parallel * p->ef;
+    int64_t capS = std::min<int64_t>(capF * G->max_deg, (int64_t)p->k_parallel * G->dg.n);
+    capS = std::max<int64_t>(capS, G->max_deg + 1) + 64;
+    const int64_t capP = p->k + capS;
+    if (int rc = ensure_search_scratch(S, G, slots, capF, capS, capP)) return rc;
+    a.g = G->dg;
+    a.Q = Q;
+    a.k = p->k;
+    a.kp = p->k_parallel;
+    a.hops = p->hops;
+    a.ef = p->ef;
+    a.out_ids = ids;
+    a.out_scores = scores;
+    a.out_count = count;
+    a.out_stats = stats;
+    a.tags = S->tags;
+    a.epochs = S->epochs;
+    a.f_slot = S->f_slot;
+    a.f_srch = S->f_srch;
+    a.surv_v = S->surv_v;
+    a.surv_i = S->surv_i;
+    a.fr_v = S->fr_v;
+    a.fr_i = S->fr_i;
+    a.fr_key = S->fr_key;
+    a.seg_v = S->seg_v;
+    a.seg_key = S->seg_key;
+    a.pool_key = S->pool_key;
+    a.pool_slot = S->pool_slot;
+    a.pool_meta = S->pool_meta;
+    a.counters = S->counters;
+    a.phase_cycles = S->phase;
+    a.capF = S->capF;
+    a.capS = S->capS;
+    a.capP = S->capP;
+    a.queue = S->flags;
+    a.nonfinite = S->flags + 1;
+    a.tab_code = T->code;
+    a.tab_f64 = T->tab;
+    a.tab_n = T->n;
+    GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
+    kern<<<(int)slots, GR_NT, smem, stream>>>(a);
+    GR_CUDA(cudaGetLastError());
+    S->launches += 1;
+    return GR_OK;
+}
+
 } // namespace
+
 
 extern "C" {
 
@@ -1156,6 +1216,132 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
         GR_CUDA(cudaMemcpyAsync(out_stats, s->st_stats.p, ns * 8, cudaMemcpyDeviceToHost, st));
     }
     return gr_searcher_status(s, stream);
+}
+
+// ------------------------------------------------------------------ score tables
+namespace {
+int scores_finish(gr_scores *T, int *bad, cudaStream_t st, gr_scores **out) {
+    cudaError_t e = build_score_codes(T->tab, T->Q, T->n, T->code, bad, st);
+    int hbad = 0;
+    if (e == cudaSuccess) e = cudaMemcpy(&hbad, bad, 4, cudaMemcpyDeviceToHost);
+    cudaFree(bad);
+    if (e != cudaSuccess) {
+        gr_scores_destroy(T);
+        return fail(GR_ECUDA, std::string("score table: ") + cudaGetErrorString(e));
+    }
+    if (hbad) {
+        gr_scores_destroy(T);
+        return fail(GR_ENUMERIC, "NaN in score table");
+    }
+    *out = T;
+    return GR_OK;
+}
+int scores_alloc(int device, int64_t Q, int64_t n, gr_scores **T, int **bad) {
+    if (Q < 1 || n < 1) return fail(GR_EINVAL, "empty score table");
+    if (n >= (int64_t)1 << 31) return fail(GR_EINVAL, "score table wider than 2^31 items");
+    GR_CUDA(cudaSetDevice(device));
+    gr_scores *t = new gr_scores();
+    t->device = device;
+    t->Q = Q;
+    t->n = n;
+    int rc = dmalloc(&t->tab, (size_t)(Q * n));
+    if (!rc) rc = dmalloc(&t->code, (size_t)(Q * n));
+    if (!rc) rc = dmalloc(bad, 1);
+    if (rc) { gr_scores_destroy(t); return rc; }
+    cudaMemset(*bad, 0, 4);
+    *T = t;
+    return GR_OK;
+}
+} // namespace
+
+int gr_scores_create(int device, const double *table, int64_t Q, int64_t n_items, int on_device,
+                     gr_scores **out) {
+    if (!table || !out) return fail(GR_EINVAL, "null argument");
+    gr_scores *T = nullptr;
+    int *bad = nullptr;
+    if (int rc = scores_alloc(device, Q, n_items, &T, &bad)) return rc;
+    const cudaError_t e = cudaMemcpy(T->tab, table, (size_t)(Q * n_items) * 8,
+                                     on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) { cudaFree(bad); gr_scores_destroy(T); return fail(GR_ECUDA, cudaGetErrorString(e)); }
+    return scores_finish(T, bad, 0, out);
+}
+
+int gr_scores_euclid(int device, const double *vectors, int64_t n_items, int32_t dim,
+                     const double *queries, int64_t Q, gr_scores **out) {
+    if (!vectors || !queries || !out) return fail(GR_EINVAL, "null argument");
+    if (dim < 1) return fail(GR_EINVAL, "dim must be >= 1");
+    gr_scores *T = nullptr;
+    int *bad = nullptr;
+    if (int rc = scores_alloc(device, Q, n_items, &T, &bad)) return rc;
+    double *dv = nullptr, *dq = nullptr;
+    int rc = dmalloc(&dv, (size_t)(n_items * dim));
+    if (!rc) rc = dmalloc(&dq, (size_t)(Q * dim));
+    if (rc) { cudaFree(dv); cudaFree(bad); gr_scores_destroy(T); return rc; }
+    cudaMemcpy(dv, vectors, (size_t)(n_items * dim) * 8, cudaMemcpyHostToDevice);
+    cudaMemcpy(dq, queries, (size_t)(Q * dim) * 8, cudaMemcpyHostToDevice);
+    const int64_t total = Q * n_items;
+    euclid_table_kernel<<<(unsigned)std::min<int64_t>((total + 255) / 256, 148 * 16), 256>>>(
+        dv, n_items, dim, dq, Q, T->tab, bad);
+    const cudaError_t e = cudaDeviceSynchronize();
+    cudaFree(dv);
+    cudaFree(dq);
+    if (e != cudaSuccess) { cudaFree(bad); gr_scores_destroy(T); return fail(GR_ECUDA, cudaGetErrorString(e)); }
+    return scores_finish(T, bad, 0, out);
+}
+
+int gr_scores_destroy(gr_scores *t) {
+    if (!t) return GR_OK;
+    cudaSetDevice(t->device);
+    cudaFree(t->tab);
+    cudaFree(t->code);
+    delete t;
+    return GR_OK;
+}
+
+int gr_scores_read(const gr_scores *t, double *out) {
+    if (!t || !out) return fail(GR_EINVAL, "null argument");
+    GR_CUDA(cudaSetDevice(t->device));
+    GR_CUDA(cudaMemcpy(out, t->tab, (size_t)(t->Q * t->n) * 8, cudaMemcpyDeviceToHost));
+    return GR_OK;
+}
+
+int gr_search_scores(gr_searcher *s, const gr_graph *g, const gr_scores *t,
+                     const gr_search_params *p, int64_t *out_ids, double *out_scores,
+                     int32_t *out_count, int64_t *out_stats, int on_device, void *stream) {
+    if (!s || !g || !t || !out_ids || !out_scores || !out_count || !out_stats)
+        return fail(GR_EINVAL, "null argument");
+    if (int rc = check_params(p)) return rc;
+    if (p->mode != GR_MODE_EXACT) return fail(GR_EINVAL, "score tables are exact-mode only");
+    if (t->device != s->device || g->device != s->device) return fail(GR_EINVAL, "handles on different devices");
+    GR_CUDA(cudaSetDevice(s->device));
+    {   // every item id must index the table (ids = score-table columns, search.py:79)
+        std::vector<int64_t> hid(g->dg.n);
+        GR_CUDA(cudaMemcpy(hid.data(), g->dg.ids, g->dg.n * 8, cudaMemcpyDeviceToHost));
+        for (int64_t v : hid)
+            if (v < 0 || v >= t->n) return fail(GR_EINVAL, "graph item id outside the score table");
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t Q = t->Q, no = Q * p->k, ns = Q * (5 + g->dg.n_layers);
+    if (on_device)
+        return launch_search_scores(s, g, t, p, out_ids, out_scores, out_count, out_stats, st);
+    int64_t *di = nullptr, *dst = nullptr;
+    double *ds = nullptr;
+    int32_t *dc = nullptr;
+    int rc = dmalloc(&di, (size_t)no);
+    if (!rc) rc = dmalloc(&ds, (size_t)no);
+    if (!rc) rc = dmalloc(&dc, (size_t)Q);
+    if (!rc) rc = dmalloc(&dst, (size_t)ns);
+    if (!rc) rc = launch_search_scores(s, g, t, p, di, ds, dc, dst, st);
+    if (!rc) {
+        cudaMemcpyAsync(out_ids, di, no * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out_scores, ds, no * 8, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out_count, dc, Q * 4, cudaMemcpyDeviceToHost, st);
+        cudaMemcpyAsync(out_stats, dst, ns * 8, cudaMemcpyDeviceToHost, st);
+        const cudaError_t e = cudaStreamSynchronize(st);
+        if (e != cudaSuccess) rc = fail(GR_ECUDA, cudaGetErrorString(e));
+    }
+    cudaFree(di); cudaFree(ds); cudaFree(dc); cudaFree(dst);
+    return rc;
 }
 
 // ------------------------------------------------------------------ pairs

@@ -59,6 +59,10 @@ struct SearchArgs {
     int off_w0, off_w[GR_MAX_MLP], off_b[GR_MAX_MLP], off_A, off_acc0, off_x0, off_h0, off_h1,
         off_score, off_hist, off_sortk, off_sortv, off_kp;
     int ldx0, ldh, sortcap;
+    // MODE 2 (traversal-only score table, scores.cuh): codes / fp64 scores [Q][tab_n] by item id
+    const uint32_t *tab_code;
+    const double *tab_f64;
+    int64_t tab_n;
 };
 
 struct CtaState {
@@ -258,7 +262,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         const float *hu = a.users + q * d_h;
 
         // ---- hoisted user-half accumulators of layer 0
-        for (int o = tid; o < O0; o += GR_NT) {
+        for (int o = tid; o < (MODE == 2 ? 0 : O0); o += GR_NT) {
             float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
             for (int j = 0; j < pre; ++j) {
                 const int c = chunk_perm(j, K0);
@@ -275,6 +279,34 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
         auto score_fresh = [&](int nFresh, int hop) {
             const int pc = st.pool_cur;
             const uint64_t poolT = st.poolT;
+            if constexpr (MODE == 2) {
+                // score-table lookup: key = dense rank of the fp64 score << 32 | ~id rank
+                const uint32_t *crow = a.tab_code + q * a.tab_n;
+                for (int i0 = 0; i0 < nFresh; i0 += GR_NT) {
+                    const int i = i0 + tid;
+                    uint64_t key = 0ull;
+                    int32_t s = 0;
+                    if (i < nFresh) {
+                        s = fr_v[i];
+                        key = ((uint64_t)__ldg(crow + g.ids[s]) << 32) | (uint64_t)(~slot_rank(g, s));
+                        fr_key[i] = key;
+                        if (key > poolT) {
+                            const int idx = atomicAdd(&st.nPool, 1);
+                            pkey[pc][idx] = key;
+                            pslot[pc][idx] = s;
+                        }
+                    }
+                    uint64_t mx = key;
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) {
+                        const uint64_t y = __shfl_xor_sync(0xffffffffu, mx, o);
+                        mx = y > mx ? y : mx;
+                    }
+                    if (lane == 0 && mx) atomicMax(reinterpret_cast<unsigned long long *>(&st.hopmax), mx);
+                }
+                __syncthreads();
+                return;
+            }
             if constexpr (MODE == 1) {
                 // approximate scores on the tensor cores, 128 pairs per tile
                 const float Ts = orderable_f32((uint32_t)(poolT >> 32));
@@ -682,7 +714,10 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
             for (int j = tid; j < a.k; j += GR_NT) {
                 if (j < nr) {
                     a.out_ids[q * a.k + j] = g.ids[sortv[j]];
-                    a.out_scores[q * a.k + j] = (double)orderable_f32((uint32_t)(sortk[j] >> 32));
+                    if constexpr (MODE == 2)
+                        a.out_scores[q * a.k + j] = a.tab_f64[q * a.tab_n + g.ids[sortv[j]]];
+                    else
+                        a.out_scores[q * a.k + j] = (double)orderable_f32((uint32_t)(sortk[j] >> 32));
                 } else {
                     a.out_ids[q * a.k + j] = -1;
                     a.out_scores[q * a.k + j] = __longlong_as_double(0x7ff8000000000000ll);

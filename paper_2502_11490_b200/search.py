@@ -134,6 +134,53 @@ def model_scorer(model, user_embedding: np.ndarray, item_embeddings: np.ndarray)
     return ModelScorer(model, user_embedding, item_embeddings)
 
 
+class EuclideanScorer:
+    """ScoreFn of ``euclidean_scorer`` (search.py:73-81): -||v - q|| in fp64, item ids are
+    row indexes.  Scores come from the device (gr_scores_euclid, numpy's fp64 einsum order,
+    bit-exact); ``c_hipanns`` runs the traversal on the device over that score table."""
+
+    def __init__(self, query, item_vectors):
+        self.query = np.asarray(query, dtype=np.float64).reshape(-1)
+        self.vectors = np.asarray(item_vectors)
+        self._table = None
+
+    def device_scores(self, device: int | None = None) -> _lib.DeviceScores:
+        if self._table is None:
+            self._table = _lib.DeviceScores(vectors=self.vectors, queries=self.query[None, :],
+                                            device=device)
+        return self._table
+
+    def __call__(self, ids: np.ndarray) -> np.ndarray:
+        ids = np.asarray(ids, dtype=np.int64)
+        return self.device_scores().read()[0][ids]
+
+
+def euclidean_scorer(query: np.ndarray, item_vectors: np.ndarray) -> ScoreFn:
+    """Score = negated Euclidean distance; item ids must be row indexes."""
+    return EuclideanScorer(query, item_vectors)
+
+
+class TableScorer:
+    """A ScoreFn given as its fp64 values over item ids 0..n-1 (``scores[id]``): the
+    traversal-only form of an arbitrary ScoreFn (search.py:27) the device can run."""
+
+    def __init__(self, scores):
+        self.scores = np.ascontiguousarray(scores, dtype=np.float64).reshape(-1)
+        self._table = None
+
+    def device_scores(self, device: int | None = None) -> _lib.DeviceScores:
+        if self._table is None:
+            self._table = _lib.DeviceScores(self.scores[None, :], device=device)
+        return self._table
+
+    def __call__(self, ids: np.ndarray) -> np.ndarray:
+        return self.scores[np.asarray(ids, dtype=np.int64)]
+
+
+def table_scorer(scores: np.ndarray) -> ScoreFn:
+    return TableScorer(scores)
+
+
 # ------------------------------------------------------------------ batched search
 @dataclass
 class BatchSearchResult:
@@ -208,6 +255,35 @@ def c_hipanns_batch(index: GraphIndex, model, users, item_embeddings,
                              hops_to_best=stats[:, 2], per_layer=stats[:, 5:], wall_time_s=wall)
 
 
+def c_hipanns_scores_batch(index: GraphIndex, scores, params: SearchParams,
+                           device: int | None = None,
+                           searcher: _lib.DeviceSearcher | None = None) -> BatchSearchResult:
+    """C-HiPANNS for every row of a score table (``DeviceScores`` or an fp64 array
+    [Q, n_items] by item id): traversal-only mode used by the reference's search tests."""
+    if len(index) == 0:
+        raise InvalidArgumentError("index is empty")
+    if params.mode != "exact":
+        raise InvalidArgumentError("score tables run in exact mode only")
+    device = _lib.current_device() if device is None else device
+    if not isinstance(scores, _lib.DeviceScores):
+        scores = _lib.DeviceScores(scores, device=device)
+    g = index.device_graph(device)
+    s = searcher or _searcher(device)
+    Q, k, L = scores.Q, params.k, g.n_layers
+    ids = np.empty((Q, k), dtype=np.int64)
+    sc = np.empty((Q, k), dtype=np.float64)
+    count = np.empty(Q, dtype=np.int32)
+    stats = np.empty((Q, 5 + L), dtype=np.int64)
+    pc = params._c()
+    t0 = time.perf_counter()
+    _lib.check(_lib.lib().gr_search_scores(s.h, g.h, scores.h, ctypes.byref(pc), _lib.ptr(ids),
+                                           _lib.ptr(sc), _lib.ptr(count), _lib.ptr(stats), 0, None))
+    wall = time.perf_counter() - t0
+    return BatchSearchResult(ids=ids, scores=sc, count=count, evals=stats[:, 0],
+                             rows_expanded=stats[:, 3], nbr_ids_read=stats[:, 4],
+                             hops_to_best=stats[:, 2], per_layer=stats[:, 5:], wall_time_s=wall)
+
+
 def c_hipanns(index: GraphIndex, score_fn: ScoreFn, params: SearchParams) -> SearchResult:
     """Breadth-parallel layered search with a shared candidate pool (search.py:194-286).
 
@@ -218,9 +294,12 @@ def c_hipanns(index: GraphIndex, score_fn: ScoreFn, params: SearchParams) -> Sea
     """
     if len(index) == 0:
         raise InvalidArgumentError("index is empty")
+    if isinstance(score_fn, (EuclideanScorer, TableScorer)):
+        return c_hipanns_scores_batch(index, score_fn.device_scores(), params).result(0)
     if not isinstance(score_fn, ModelScorer):
         raise InvalidArgumentError(
-            "c_hipanns runs on the GPU: score_fn must come from model_scorer(...) "
+            "c_hipanns runs on the GPU: score_fn must come from model_scorer(...), "
+            "euclidean_scorer(...) or table_scorer(...) "
             "(there is no CPU fallback for arbitrary callables)")
     r = c_hipanns_batch(index, score_fn.model, score_fn.user[None, :], score_fn.items, params)
     return r.result(0)
@@ -249,11 +328,13 @@ def brute_force(score_fn: ScoreFn, item_ids: Sequence[int], k: int) -> SearchRes
     item_ids = np.asarray(item_ids, dtype=np.int64)
     if k > len(item_ids):
         raise InvalidArgumentError(f"k={k} exceeds item count {len(item_ids)}")
-    if not isinstance(score_fn, ModelScorer):
-        raise InvalidArgumentError("brute_force runs on the GPU: use model_scorer(...)")
+    if not isinstance(score_fn, (ModelScorer, EuclideanScorer, TableScorer)):
+        raise InvalidArgumentError("brute_force runs on the GPU: use model_scorer(...), "
+                                   "euclidean_scorer(...) or table_scorer(...)")
     t0 = time.perf_counter()
-    n_items = score_fn.items.shape[0]
-    if len(item_ids) == n_items and np.array_equal(item_ids, np.arange(n_items)):
+    n_items = score_fn.items.shape[0] if isinstance(score_fn, ModelScorer) else -1
+    if isinstance(score_fn, ModelScorer) and len(item_ids) == n_items and \
+            np.array_equal(item_ids, np.arange(n_items)):
         ids, scores = brute_force_batch(score_fn.model, score_fn.user[None, :], score_fn.items, k)
         items = [(int(i), float(s)) for i, s in zip(ids[0], scores[0])]
     else:

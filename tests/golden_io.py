@@ -45,3 +45,44 @@ def expected(z, pi):
 
 
 SEARCH_FIXTURES = ["search_d64_z2", "search_d128_z3", "search_d32_shuffled"]
+
+
+# ---- tests/golden/reftests.npz: the reference's own test_search.py cases (make_reftests.py)
+class RefCase:
+    """One recorded case: graph arrays, fp64 vectors/queries, per-parameter-set results."""
+
+    def __init__(self, z, name: str):
+        self.name = name
+        p = name + "/"
+        self.z, self.p = z, p
+        self.vectors = z[p + "vectors"]
+        self.queries = z[p + "queries"]
+        self.ids = z[p + "ids"]
+        self.levels = z[p + "levels"]
+        self.entry = int(z[p + "entry_slot"])
+        self.m = int(z[p + "m"])
+        self.layers = [(z[p + f"nbrs{l}"], z[p + f"cnts{l}"]) for l in range(int(z[p + "n_layers"]))]
+        self.bf_ids = z[p + "bf_ids"]
+        self.bf_scores = z[p + "bf_scores"]
+
+    def params(self):
+        out, i = [], 0
+        while f"{self.p}p{i}/params" in self.z.files:
+            k, kp, hops, ef = (int(v) for v in self.z[f"{self.p}p{i}/params"])
+            out.append((i, dict(k=k, k_parallel=kp, hops=hops, ef=ef)))
+            i += 1
+        return out
+
+    def expected(self, pi):
+        pp = f"{self.p}p{pi}/"
+        return {k: self.z[pp + k] for k in ("ids", "scores", "n", "evals", "per_layer", "best_hop")}
+
+
+def ref_cases(prefix: str = ""):
+    z = load("reftests")
+    names = sorted({k.split("/")[0] for k in z.files if k.endswith("/entry_slot")})
+    return [n for n in names if n.startswith(prefix)]
+
+
+def ref_case(name: str) -> RefCase:
+    return RefCase(load("reftests"), name)

@@ -109,3 +109,21 @@ def test_c_oracle_search_matches_reference(fixture):
         np.testing.assert_array_equal(r["per_layer"], exp["per_layer"])
         np.testing.assert_array_equal(r["rows"], exp["rows"])
         np.testing.assert_array_equal(r["nbr_ids"], exp["nbr_ids"])
+
+
+@pytest.mark.parametrize("case", G.ref_cases())
+def test_oracle_reproduces_reference_search_tests(case):
+    """The reference's own test_search.py cases (make_reftests.py): the numpy oracle's
+    euclidean scorer + hop-synchronous c_hipanns give the reference's items and counts."""
+    c = G.ref_case(case)
+    graph = O.OracleGraph(c.layers, c.entry, c.ids)
+    for pi, p in c.params():
+        exp = c.expected(pi)
+        for q in range(len(c.queries)):
+            r = O.c_hipanns(graph, lambda s, q=q: O.neg_euclid_f64(c.vectors, c.queries[q], s), **p)
+            n = int(exp["n"][q])
+            assert [i for i, _ in r["items"]] == list(exp["ids"][q, :n])
+            assert [s for _, s in r["items"]] == list(exp["scores"][q, :n])
+            assert r["evals"] == exp["evals"][q]
+            assert r["per_layer"] == list(exp["per_layer"][q])
+            assert r["hops_to_best"] == exp["best_hop"][q]

@@ -44,6 +44,10 @@ def main():
     pc = SearchParams(**kw)._c()
     lib = _lib.lib()
     st = ctypes.c_void_p(torch.cuda.current_stream().cuda_stream)
+    # ncu --profile-from-start off: only the search launches are profiled (the workload
+    # builder's thousands of small kernels stay outside the capture range)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.start()
     for r in range(reps):
         torch.cuda.synchronize()
         t0 = time.perf_counter()
@@ -54,6 +58,7 @@ def main():
         stats = ost.cpu().numpy()
         print(f"launch {r}: {dt*1e3:.2f} ms  {Q/dt:.0f} q/s  evals/q {stats[:,0].mean():.1f} "
               f"rows/q {stats[:,3].mean():.1f} nbrs/q {stats[:,4].mean():.1f}", flush=True)
+    torch.cuda.profiler.stop()
     print("counters", s.counters(), flush=True)
 
 
