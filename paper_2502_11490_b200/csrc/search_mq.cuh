@@ -818,48 +818,86 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                 const int fc = st.f_cur;
                 if (tid == 0) { st.nS = 0; st.nFresh = 0; }
                 __syncthreads();
-                // ---- expand + claim: 8 frontier rows per warp, all row loads then all claim
-                // atomics issued back-to-back (the ballots that consume them come after)
-                constexpr int R = 8;
-                for (int e0 = warp * R; e0 < nF; e0 += NW * R) {
-                    int32_t s[R], gi[R];
-                    const int32_t *row[R];
+                // ---- expand + claim.  A warp takes RW frontier rows and spreads their 16-byte
+                // pieces over the lanes (<= 4 per lane): every row load is in flight at once,
+                // then every claim atomic, then ONE aggregated survivor append per warp.
+                {
+                    const int P = g.ld[layer] >> 2;           // int4 pieces per row
+                    const int RW = min(32, 128 / P), NP = RW * P;
+                    constexpr unsigned FULL = 0xffffffffu;
+                    for (int e0 = warp * RW; e0 < nF; e0 += NW * RW) {
+                        int32_t ms = -1, mgi = 0;
+                        if (lane < RW && e0 + lane < nF) { ms = fslot[fc][e0 + lane]; mgi = fsrch[fc][e0 + lane]; }
+                        const int4 *mrow = ms >= 0 ? reinterpret_cast<const int4 *>(graph_row(g, layer, ms)) : nullptr;
+                        int4 pv[4];
+                        int pgi[4];
 #pragma unroll
-                    for (int u = 0; u < R; ++u) {
-                        const int e = e0 + u;
-                        s[u] = e < nF ? fslot[fc][e] : -1;
-                        gi[u] = e < nF ? fsrch[fc][e] : 0;
-                    }
+                        for (int j = 0; j < 4; ++j) {
+                            const int pc = lane + 32 * j, r = min(pc / P, 31), c = pc - r * P;
+                            const int4 *rp = reinterpret_cast<const int4 *>(
+                                __shfl_sync(FULL, reinterpret_cast<unsigned long long>(mrow), r));
+                            pgi[j] = __shfl_sync(FULL, mgi, r);
+                            pv[j] = (pc < NP && rp) ? __ldg(rp + c) : make_int4(-1, -1, -1, -1);
+                        }
+                        uint32_t old[4][4];
+                        int cnt = 0, nv = 0;
 #pragma unroll
-                    for (int u = 0; u < R; ++u) row[u] = s[u] >= 0 ? graph_row(g, layer, s[u]) : nullptr;
-                    int nvalid[R];
+                        for (int j = 0; j < 4; ++j) {
+                            const int gq = pgi[j] >> 16;
+                            const uint32_t code = claim_code(st.qs[gq].epoch, pgi[j] & 0xFFFF);
+                            uint32_t *tg = tags_of(gq);
+                            const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
-                    for (int u = 0; u < R; ++u) nvalid[u] = 0;
-                    for (int c0 = 0; c0 < deg; c0 += 32) {
-                        int32_t v[R];
-                        uint32_t old[R], code[R];
-#pragma unroll
-                        for (int u = 0; u < R; ++u)
-                            v[u] = (row[u] && c0 + lane < deg) ? __ldg(row[u] + c0 + lane) : -1;
-#pragma unroll
-                        for (int u = 0; u < R; ++u) {
-                            code[u] = claim_code(st.qs[gi[u] >> 16].epoch, gi[u] & 0xFFFF);
-                            old[u] = v[u] >= 0 ? atomicMax(tags_of(gi[u] >> 16) + v[u], code[u]) : 0xFFFFFFFFu;
+                            for (int u = 0; u < 4; ++u) old[j][u] = vv[u] >= 0 ? atomicMax(tg + vv[u], code) : 0xFFFFFFFFu;
                         }
 #pragma unroll
-                        for (int u = 0; u < R; ++u) {
-                            nvalid[u] += __popc(__ballot_sync(0xffffffffu, v[u] >= 0));
-                            warp_append2(v[u] >= 0 && old[u] < code[u], v[u], gi[u], &st.nS, surv_v, surv_i);
-                        }
-                    }
-                    if (lane == 0) {
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t code = claim_code(st.qs[pgi[j] >> 16].epoch, pgi[j] & 0xFFFF);
+                            const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
-                        for (int u = 0; u < R; ++u)
-                            if (s[u] >= 0) {
-                                MqQuery &Q = st.qs[gi[u] >> 16];
-                                atomicAdd(&Q.rows, 1);
-                                atomicAdd(&Q.nbrs, nvalid[u]);
+                            for (int u = 0; u < 4; ++u) {
+                                nv += vv[u] >= 0;
+                                cnt += (vv[u] >= 0 && old[j][u] < code);
                             }
+                        }
+                        // one survivor reservation per warp (inclusive scan of the lane counts)
+                        int incl = cnt;
+#pragma unroll
+                        for (int o = 1; o < 32; o <<= 1) {
+                            const int y = __shfl_up_sync(FULL, incl, o);
+                            if (lane >= o) incl += y;
+                        }
+                        int base = 0;
+                        if (lane == 31 && incl) base = atomicAdd(&st.nS, incl);
+                        base = __shfl_sync(FULL, base, 31) + incl - cnt;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint32_t code = claim_code(st.qs[pgi[j] >> 16].epoch, pgi[j] & 0xFFFF);
+                            const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
+#pragma unroll
+                            for (int u = 0; u < 4; ++u)
+                                if (vv[u] >= 0 && old[j][u] < code) {
+                                    surv_v[base] = vv[u];
+                                    surv_i[base] = pgi[j];
+                                    ++base;
+                                }
+                        }
+                        // stats: rows expanded / neighbour ids read per query (usually one
+                        // query per warp iteration: one reduction + one atomic)
+                        const int gq0 = __shfl_sync(FULL, mgi, 0) >> 16;
+                        if (__all_sync(FULL, ms < 0 || (mgi >> 16) == gq0)) {
+                            int nrow = __popc(__ballot_sync(FULL, ms >= 0)), tot = nv;
+#pragma unroll
+                            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
+                            if (lane == 0) { atomicAdd(&st.qs[gq0].rows, nrow); atomicAdd(&st.qs[gq0].nbrs, tot); }
+                        } else {
+                            if (ms >= 0) atomicAdd(&st.qs[mgi >> 16].rows, 1);
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const int n4 = (pv[j].x >= 0) + (pv[j].y >= 0) + (pv[j].z >= 0) + (pv[j].w >= 0);
+                                if (n4) atomicAdd(&st.qs[pgi[j] >> 16].nbrs, n4);
+                            }
+                        }
                     }
                 }
                 __syncthreads();

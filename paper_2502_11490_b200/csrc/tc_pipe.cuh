@@ -83,7 +83,7 @@ struct TcPipe {
         if (T == 0) return;
         // role timers (GMPGR_PHASE_TIMING): one writer thread per slot
         //   0 E layer-0 epilogue  1 E layer-1 epilogue  2 E d0full-wait  3 E d1full-wait  4 E total
-        //   5 issuer full-wait   6 issuer a1full-wait  7 loader empty-wait
+        //   5 issuer idle (polling, nothing ready)  7 loader empty-wait
         const long long t_run = sub ? clock64() : 0;
 #define TP_WAIT(slot, expr)                                                   \
     do {                                                                      \
@@ -136,49 +136,66 @@ struct TcPipe {
                 }
             }
         } else if (warp == ISSUER_WARP) {
-            // ================= MMA issuer (one thread)
+            // ================= MMA issuer (one thread): polls the barriers and issues
+            // whatever is ready -- layer 1 of an earlier tile as soon as its A1 operand is in
+            // TMEM, else the next layer-0 K chunk -- so neither waits behind the other
             if (lane == 0) {
                 const uint32_t bH0 = tc::smem_u32(sm + OFF_B0H), bL0 = tc::smem_u32(sm + OFF_B0L);
                 const uint32_t bH1 = tc::smem_u32(sm + OFF_B1H), bL1 = tc::smem_u32(sm + OFF_B1L);
-                auto layer1 = [&](int t) {
-                    const uint32_t tg = tile_ctr + t, e = tg & 1u, v = tg >> 1;
-                    TP_WAIT(6, tc::mbar_wait(bar(sm, A1FULL0 + e), v & 1u));
-                    tc::fence_after();
-                    const uint32_t a1 = tmem + C_A1 + 64 * e, d1 = tmem + C_D1 + 64 * e;
+                int l0t = 0, l0k = 0, l1t = 0;
+                long long idle0 = 0;
+                while (l1t < T) {
+                    if (l1t < l0t) {
+                        const uint32_t tg = tile_ctr + l1t, e = tg & 1u, v = tg >> 1;
+                        if (tc::mbar_test(bar(sm, A1FULL0 + e), v & 1u)) {
+                            tc::fence_after();
+                            const uint32_t a1 = tmem + C_A1 + 64 * e, d1 = tmem + C_D1 + 64 * e;
 #pragma unroll
-                    for (int k = 0; k < H / 16; ++k) {
-                        const uint64_t bh = tc::desc(bH1 + k * 256, H), bl = tc::desc(bL1 + k * 256, H);
-                        tc::mma_ts(d1, a1 + k * 8, bh, IDESC, k ? 1u : 0u);  // hi . hi
-                        tc::mma_ts(d1, a1 + k * 8, bl, IDESC, 1u);           // hi . lo
-                        tc::mma_ts(d1, a1 + 32 + k * 8, bh, IDESC, 1u);      // lo . hi
+                            for (int k = 0; k < H / 16; ++k) {
+                                const uint64_t bh = tc::desc(bH1 + k * 256, H), bl = tc::desc(bL1 + k * 256, H);
+                                tc::mma_ts(d1, a1 + k * 8, bh, IDESC, k ? 1u : 0u);  // hi . hi
+                                tc::mma_ts(d1, a1 + k * 8, bl, IDESC, 1u);           // hi . lo
+                                tc::mma_ts(d1, a1 + 32 + k * 8, bh, IDESC, 1u);      // lo . hi
+                            }
+                            tc::commit(bar(sm, D1FULL0 + e));
+                            ++l1t;
+                            idle0 = 0;
+                            continue;
+                        }
                     }
-                    tc::commit(bar(sm, D1FULL0 + e));
-                };
-                for (int t = 0; t <= T; ++t) {
-                    if (t < T) {
-                        const uint32_t tg = tile_ctr + t, e = tg & 1u, v = tg >> 1;
-                        if (v >= 1) tc::mbar_wait(bar(sm, D0EMPTY0 + e), (v - 1) & 1u);
-                        const uint32_t d0 = tmem + C_D0 + 64 * e;
-                        for (int kc = 0; kc < NC; ++kc) {
-                            const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, u = qg / S;
-                            TP_WAIT(5, tc::mbar_wait(bar(sm, FULL0 + s), u & 1u));
+                    bool issued = false;
+                    if (l0t < T) {
+                        const uint32_t tg = tile_ctr + l0t, e = tg & 1u, v = tg >> 1;
+                        const uint32_t qg = chunk_ctr + l0t * NC + l0k, s = qg % S, u = qg / S;
+                        if ((l0k != 0 || v == 0 || tc::mbar_test(bar(sm, D0EMPTY0 + e), (v - 1) & 1u)) &&
+                            tc::mbar_test(bar(sm, FULL0 + s), u & 1u)) {
                             tc::fence_async_smem();
                             tc::fence_after();
+                            const uint32_t d0 = tmem + C_D0 + 64 * e;
                             const uint32_t aH = tc::smem_u32(sm + OFF_A + s * 2 * CH_BYTES), aL = aH + CH_BYTES;
 #pragma unroll
                             for (int k = 0; k < KC / 16; ++k) {
                                 const uint64_t ah = tc::desc(aH + k * 256, KC), al = tc::desc(aL + k * 256, KC);
-                                const uint32_t kb = (kc * (KC / 16) + k) * 256;
+                                const uint32_t kb = (l0k * (KC / 16) + k) * 256;
                                 const uint64_t bh = tc::desc(bH0 + kb, D_H), bl = tc::desc(bL0 + kb, D_H);
-                                tc::mma(d0, ah, bh, IDESC, (kc | k) ? 1u : 0u);
+                                tc::mma(d0, ah, bh, IDESC, (l0k | k) ? 1u : 0u);
                                 tc::mma(d0, ah, bl, IDESC, 1u);
                                 tc::mma(d0, al, bh, IDESC, 1u);
                             }
                             tc::commit(bar(sm, EMPTY0 + s));
+                            if (++l0k == NC) {
+                                tc::commit(bar(sm, D0FULL0 + e));
+                                l0k = 0;
+                                ++l0t;
+                            }
+                            issued = true;
                         }
-                        tc::commit(bar(sm, D0FULL0 + e));
                     }
-                    if (t >= 1) layer1(t - 1);
+                    if (sub) {  // issuer idle time (no barrier ready)
+                        const long long now = clock64();
+                        if (!issued && idle0) sub[5] += (unsigned long long)(now - idle0);
+                        idle0 = issued ? 0 : now;
+                    }
                 }
             }
             __syncwarp();
