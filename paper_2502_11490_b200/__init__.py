@@ -6,7 +6,17 @@ sm_100a kernels for the hop-synchronous C-HiPANNS traversal with fused exact-fp3
 metric scoring, the pair scorer, exact brute force and the shard top-k merge.
 """
 
-from .batching import BatchEngine, GpuBatchEngine
+from .batching import (
+    BatchClient,
+    BatchEngine,
+    BatchQueue,
+    Dispatcher,
+    DispatchStats,
+    EvalRequest,
+    GpuBatchEngine,
+    ModelBatchEngine,
+    run_dispatcher,
+)
 from .errors import (
     DeviceError,
     FileFormatError,
@@ -50,7 +60,8 @@ from .search import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "BatchEngine", "BatchSearchResult", "CandidatePool", "DeviceError", "FileFormatError",
+    "BatchClient", "BatchEngine", "BatchQueue", "BatchSearchResult", "DispatchStats", "Dispatcher",
+    "EvalRequest", "ModelBatchEngine", "run_dispatcher", "CandidatePool", "DeviceError", "FileFormatError",
     "GpuBatchEngine", "GraphIndex", "InvalidArgumentError", "MetricModel", "NannError",
     "NumericError", "Projector", "QueueShutdownError", "RelevanceModel", "SearchParams",
     "SearchResult", "SearchStats", "WeightOverflowError", "brute_force", "brute_force_batch",
