@@ -819,30 +819,42 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                 if (tid == 0) { st.nS = 0; st.nFresh = 0; }
                 __syncthreads();
                 // ---- expand + claim.  A warp takes RW frontier rows and spreads their 16-byte
-                // pieces over the lanes (<= 4 per lane): every row load is in flight at once,
+                // pieces over the lanes (<= 3 per lane): every row load is in flight at once,
                 // then every claim atomic, then ONE aggregated survivor append per warp.
+                // Software-pipelined: the next batch's frontier entries and row pieces are
+                // fetched while this batch's claim atomics are in flight.
                 {
                     const int P = g.ld[layer] >> 2;           // int4 pieces per row
-                    const int RW = min(32, 128 / P), NP = RW * P;
+                    const int RW = min(32, 96 / P), NP = RW * P;
                     constexpr unsigned FULL = 0xffffffffu;
-                    for (int e0 = warp * RW; e0 < nF; e0 += NW * RW) {
-                        int32_t ms = -1, mgi = 0;
+                    auto meta = [&](int e0, int32_t &ms, int32_t &mgi) {
+                        ms = -1;
+                        mgi = 0;
                         if (lane < RW && e0 + lane < nF) { ms = fslot[fc][e0 + lane]; mgi = fsrch[fc][e0 + lane]; }
+                    };
+                    auto pieces = [&](int32_t ms, int32_t mgi, int4 (&pv)[3], int (&pgi)[3]) {
                         const int4 *mrow = ms >= 0 ? reinterpret_cast<const int4 *>(graph_row(g, layer, ms)) : nullptr;
-                        int4 pv[4];
-                        int pgi[4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < 3; ++j) {
                             const int pc = lane + 32 * j, r = min(pc / P, 31), c = pc - r * P;
                             const int4 *rp = reinterpret_cast<const int4 *>(
                                 __shfl_sync(FULL, reinterpret_cast<unsigned long long>(mrow), r));
                             pgi[j] = __shfl_sync(FULL, mgi, r);
                             pv[j] = (pc < NP && rp) ? __ldg(rp + c) : make_int4(-1, -1, -1, -1);
                         }
-                        uint32_t old[4][4];
-                        int cnt = 0, nv = 0;
+                    };
+                    int32_t ms, mgi;
+                    int4 pv[3];
+                    int pgi[3];
+                    int e0 = warp * RW;
+                    meta(e0, ms, mgi);
+                    pieces(ms, mgi, pv, pgi);
+                    for (; e0 < nF; e0 += NW * RW) {
+                        int32_t ms1, mgi1;
+                        meta(e0 + NW * RW, ms1, mgi1);
+                        uint32_t old[3][4];
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < 3; ++j) {
                             const int gq = pgi[j] >> 16;
                             const uint32_t code = claim_code(st.qs[gq].epoch, pgi[j] & 0xFFFF);
                             uint32_t *tg = tags_of(gq);
@@ -850,8 +862,12 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
 #pragma unroll
                             for (int u = 0; u < 4; ++u) old[j][u] = vv[u] >= 0 ? atomicMax(tg + vv[u], code) : 0xFFFFFFFFu;
                         }
+                        int4 pv1[3];
+                        int pgi1[3];
+                        pieces(ms1, mgi1, pv1, pgi1);
+                        int cnt = 0, nv = 0;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < 3; ++j) {
                             const uint32_t code = claim_code(st.qs[pgi[j] >> 16].epoch, pgi[j] & 0xFFFF);
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
@@ -871,7 +887,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                         if (lane == 31 && incl) base = atomicAdd(&st.nS, incl);
                         base = __shfl_sync(FULL, base, 31) + incl - cnt;
 #pragma unroll
-                        for (int j = 0; j < 4; ++j) {
+                        for (int j = 0; j < 3; ++j) {
                             const uint32_t code = claim_code(st.qs[pgi[j] >> 16].epoch, pgi[j] & 0xFFFF);
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
@@ -893,11 +909,15 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                         } else {
                             if (ms >= 0) atomicAdd(&st.qs[mgi >> 16].rows, 1);
 #pragma unroll
-                            for (int j = 0; j < 4; ++j) {
+                            for (int j = 0; j < 3; ++j) {
                                 const int n4 = (pv[j].x >= 0) + (pv[j].y >= 0) + (pv[j].z >= 0) + (pv[j].w >= 0);
                                 if (n4) atomicAdd(&st.qs[pgi[j] >> 16].nbrs, n4);
                             }
                         }
+                        ms = ms1;
+                        mgi = mgi1;
+#pragma unroll
+                        for (int j = 0; j < 3; ++j) { pv[j] = pv1[j]; pgi[j] = pgi1[j]; }
                     }
                 }
                 __syncthreads();

@@ -126,8 +126,12 @@ __device__ void cta_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap) {
 // (bar >= 1; barrier 0 is __syncthreads).  gtid: thread index inside the group.
 template <int GT>
 __device__ void group_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap, int gtid, int bar) {
+    auto sync = [&]() {
+        if constexpr (GT == 32) __syncwarp();
+        else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(GT) : "memory");
+    };
     for (int i = n + gtid; i < cap; i += GT) { keys[i] = 0ull; vals[i] = -1; }
-    asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(GT) : "memory");
+    sync();
     for (int size = 2; size <= cap; size <<= 1) {
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
             for (int i = gtid; i < cap; i += GT) {
@@ -141,7 +145,7 @@ __device__ void group_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap, i
                     }
                 }
             }
-            asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(GT) : "memory");
+            sync();
         }
     }
 }

@@ -23,7 +23,7 @@ def P():
 def oracle_scores(P, model, users, items):
     from oracle import hipanns_oracle as O
 
-    om = O.OracleModel.from_metric(model.metric)
+    om = O.OracleModel.from_metric(getattr(model, "metric", model))
     s, _ = O.relevance_f32(om, users, items)
     return s.astype(np.float64)
 
