@@ -287,13 +287,15 @@ def run_gmpgr(args):
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_search_kernel.json")))
     except Exception:
         pass
-    traffic = prof.get("dram_bytes_per_query")
+    traffic = prof.get("dram_bytes_per_query") if args.config == "cfg3" else None
     roofline = {"bound": "hbm", "achieved": achieved_gbs, "peak": pk["hbm_gbs"],
                 "unit": "GB/s", "frac": achieved_gbs / pk["hbm_gbs"],
                 "traffic": None if traffic is None else traffic * Q,
                 "algorithmic_bytes_per_launch": bytes_launch,
                 "peak_source": "MEASURED_PEAKS.json" if "_fallback" not in pk else "fallback",
-                "kernel": "hipanns_search_kernel",
+                "kernel": "hipanns_mq_kernel" if d_h in (64, 128) else "hipanns_search_kernel",
+                "traffic_source": "profiles/ncu_search_kernel.json (ncu --set full, cfg3 launch, "
+                                  "dram__bytes_read.sum + dram__bytes_write.sum per query x Q)",
                 "fp32_issue": {"achieved_tflops": flops_launch / per_launch / 1e12,
                                "peak_tflops": fp32_peak,
                                "frac": flops_launch / per_launch / 1e12 / fp32_peak,

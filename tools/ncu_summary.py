@@ -106,6 +106,38 @@ def main():
         out.write("\nstall reasons (samples):\n")
         for k, v in sorted(stalls.items(), key=lambda x: -x[1])[:12]:
             out.write(f"  {k:28s} {v:10.0f}\n")
+    # hottest CUDA source lines (warp-stall samples, correlated through -lineinfo)
+    rows = ncu_csv([rep, "--page", "source", "--print-source", "cuda,sass"])
+    cur, hdr2, agg, text, why = None, None, Counter(), {}, {}
+    for r in rows:
+        if not r:
+            continue
+        if r[0] == "File Path":
+            cur = r[1].split("/")[-1]
+            continue
+        if r[0] == "Line No":
+            hdr2 = r
+            continue
+        if r[0] == "Function Name" or hdr2 is None or not r[0]:
+            continue
+        key = (cur, int(r[0]))
+        text[key] = r[1].strip()
+        try:
+            agg[key] += float(r[4] or 0)
+            c = why.setdefault(key, Counter())
+            for i, name in enumerate(hdr2):
+                if name.startswith("stall_") and "Not Issued" not in name and r[i]:
+                    c[name] += float(r[i])
+        except ValueError:
+            pass
+    tot = sum(agg.values()) or 1.0
+    with open(prefix + "_lines.txt", "w") as out:
+        out.write("share of warp-stall samples by CUDA source line (top 40) and main stall reasons\n")
+        for key, v in agg.most_common(40):
+            c = why.get(key, Counter())
+            tw = sum(c.values()) or 1.0
+            rs = ", ".join(f"{k[6:]} {100 * x / tw:.0f}%" for k, x in c.most_common(2))
+            out.write(f"{100 * v / tot:5.2f}%  {key[0]}:{key[1]:<5d} {text[key][:70]:70s}  [{rs}]\n")
     print(json.dumps({k: summary[k] for k in ("dram_bytes_per_query", "launch_list")}, indent=1))
 
 
