@@ -116,7 +116,8 @@ def dist_setup(n_gpus):
         local = int(os.environ.get("LOCAL_RANK", str(rank)))
         torch.cuda.set_device(local)
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
-        os.environ.setdefault("NCCL_DEBUG", "WARN")  # keep stdout to the one JSON line
+        if os.environ.get("NCCL_DEBUG"):  # NCCL logs go to stderr: stdout is the one JSON line
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         return dist, rank, dist.get_world_size(), local
     torch.cuda.set_device(0)
@@ -143,10 +144,17 @@ def cpu_probe(wl, threads):
     return len(probe) / t
 
 
-def cpu_baseline(wl, target_s=15.0):
-    from oracle import oracle_c
+def host_threads() -> int:
+    """Every host core this process may run on (torchrun sets OMP_NUM_THREADS=1, which
+    must not throttle the CPU baseline)."""
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
 
-    threads = oracle_c.lib().oracle_num_threads()
+
+def cpu_baseline(wl, target_s=15.0):
+    threads = host_threads()
     qps = cpu_probe(wl, threads)
     n = int(min(len(wl.users), max(64, qps * target_s)))
     r, t = cpu_search(wl, wl.users[:n], threads)
@@ -161,9 +169,7 @@ def run_reference(args):
 
     wl = workload.make(args.config, rank=0, device=local, host_items=True)
     log(f"[reference] workload {args.config} built in {wl.build_s:.1f}s")
-    from oracle import oracle_c
-
-    threads = oracle_c.lib().oracle_num_threads()
+    threads = host_threads()
     qps = cpu_probe(wl, threads)
     per_step = int(min(len(wl.users), max(64, qps * args.ref_step_s)))
     for w in range(args.warmup):
@@ -189,6 +195,8 @@ def run_reference(args):
         "gpu_launches": 0,
     }
     print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
     return 0
 
 

@@ -277,7 +277,7 @@ class DeviceSearcher(_Handle):
             d["phase_share"] = {k: round(float(v) / tot, 4) for k, v in zip(names, out[2:10])}
             if out[10:18].any():
                 sub = ("e_epi0", "e_epi1", "e_d0full_wait", "e_d1full_wait", "e_total",
-                       "is_idle", "unused", "ld_empty_wait")
+                       "is_idle", "is_issuing", "ld_empty_wait")
                 d["pipe_share"] = {k: round(float(v) / tot, 4) for k, v in zip(sub, out[10:18])}
             elif out[10:15].any():
                 sub = ("tc_gather", "tc_mma0", "tc_epi0", "tc_mma1", "tc_epi1")

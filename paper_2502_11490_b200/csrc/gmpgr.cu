@@ -761,21 +761,37 @@ int plan_mq(int k, int kp, SearchArgs &a) {
     using TC = TcQ<DH, ZZ, NT, G, KC>;
     using TP = TcPipe<DH, ZZ, G>;
     SmemPlan P;
+    a.sortcap = pow2ceil(std::max(k, kp));
+    const int hist_b = (NT / 32) * 256 * 4, sortk_b = G * a.sortcap * 8, sortv_b = G * a.sortcap * 4;
     if (MODE == 1 && PIPE) {
         static_assert(TP::A_REGION >= EX::BUF_END * 16 || !PIPE, "exact buffers must fit the A region");
         a.off_w0 = 0;
         a.off_A = P.alloc(TP::BYTES);
-        a.off_x0 = a.off_A + TP::OFF_A;  // exact re-scoring buffers alias the A region
-    } else {
-        a.off_w0 = NT >= 512 ? P.alloc(EX::W_END * 16) : 0;
-        a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
-        a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
+        // the A-operand stages are dead outside the scoring pipeline: the exact re-scoring
+        // buffers, the radix-select histograms and the pool sort alias them when they fit
+        a.off_x0 = a.off_A + TP::OFF_A;
+        const int h = a.off_x0 + ((EX::BUF_END * 16 + 15) & ~15);
+        const int sk = h + hist_b, sv = sk + sortk_b;
+        if (sv + sortv_b <= a.off_A + TP::OFF_A + TP::A_REGION) {
+            a.off_hist = h;
+            a.off_sortk = sk;
+            a.off_sortv = sv;
+        } else {
+            a.off_hist = P.alloc(hist_b);
+            a.off_sortk = P.alloc(sortk_b);
+            a.off_sortv = P.alloc(sortv_b);
+        }
+        a.off_acc0 = P.alloc(G * 64 * 16);
+        a.off_kp = P.alloc(3 * G * kp * 4);
+        return P.bytes;
     }
+    a.off_w0 = NT >= 512 ? P.alloc(EX::W_END * 16) : 0;
+    a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
+    a.off_A = MODE == 1 ? P.alloc(TC::BYTES) : 0;
     a.off_acc0 = P.alloc(G * 64 * 16);
-    a.off_hist = P.alloc((NT / 32) * 256 * 4);
-    a.sortcap = pow2ceil(std::max(k, kp));
-    a.off_sortk = P.alloc(G * a.sortcap * 8);
-    a.off_sortv = P.alloc(G * a.sortcap * 4);
+    a.off_hist = P.alloc(hist_b);
+    a.off_sortk = P.alloc(sortk_b);
+    a.off_sortv = P.alloc(sortv_b);
     a.off_kp = P.alloc(3 * G * kp * 4);
     return P.bytes;
 }

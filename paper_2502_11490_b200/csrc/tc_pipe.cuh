@@ -4,12 +4,12 @@
 //   warps 0-7  (E, two groups of 4 warps): epilogues.  Group e owns the tiles with
 //              (global tile number & 1) == e; inside a group warp w reads TMEM lanes
 //              32*(w&3).. (one pair row per thread).
-//   warp 8     (lane 0): the single tcgen05.mma issuer
+//   warp 8     the tcgen05.mma issuer (converged warp, elect.sync picks the issuing lane)
 //   warps 9-15 (L, 224 threads): loaders.  Items carry a pre-split bf16 hi/lo copy
 //              (gr_items, [n][hi d | lo d]), so loading is pure cp.async: 16-byte pieces
 //              straight into the UMMA K-major core-matrix layout, no registers, no conversion;
 //              a cp.async.mbarrier arrival per thread completes the stage.
-// Buffers: S stages of one 64-wide K chunk of the A operand (hi + lo, 32 KB each) in shared
+// Buffers: S = 4 stages of one 64-wide K chunk of the A operand (hi + lo, 32 KB each) in shared
 // memory; in TMEM (512 columns): layer-0 accumulators D0[e] (64 cols each), layer-1
 // accumulators D1[e], and the layer-1 A operand A1[e] (relu(layer 0) as bf16 hi/lo pairs,
 // written by E with tcgen05.st and consumed by the ".ts" MMA form -- no shared memory).
@@ -26,7 +26,7 @@
 
 template <int D_H, int Z, int G>
 struct TcPipe {
-    static constexpr int H = 64, TM = 128, KC = 64, NC = D_H / KC, S = 3;
+    static constexpr int H = 64, TM = 128, KC = 64, NC = D_H / KC, S = 4;
     static constexpr int NT = 512, NE = 128, ISSUER_WARP = 8, L_WARP0 = 9, NL = NT - 32 * L_WARP0;
     // byte offsets
     static constexpr int OFF_B0H = 0;
@@ -35,7 +35,8 @@ struct TcPipe {
     static constexpr int OFF_B1L = OFF_B1H + H * H * 2;
     static constexpr int OFF_A = OFF_B1L + H * H * 2;          // S chunk stages (hi, lo)
     static constexpr int CH_BYTES = TM * KC * 2;                // one hi or lo chunk: 16 KB
-    static constexpr int A_REGION = S * 2 * CH_BYTES;           // 96 KB (aliased by exact buffers)
+    static constexpr int A_REGION = S * 2 * CH_BYTES;           // 128 KB (aliased, outside run(), by the
+                                                                // exact buffers, select histograms, pool sort)
     static constexpr int OFF_U = OFF_A + A_REGION;              // [G][64] user half + b0
     static constexpr int OFF_B1 = OFF_U + G * H * 4;
     static constexpr int OFF_W2 = OFF_B1 + H * 4;               // [Z][64]
@@ -49,7 +50,10 @@ struct TcPipe {
     static constexpr uint32_t IDESC = tc::idesc(TM, H);
     static constexpr uint32_t TMEM_COLS = 512;
     // TMEM columns ([e] at +64*e)
-    static constexpr uint32_t C_D0 = 0, C_D1 = 128, C_A1 = 256;
+    // layer-0 accumulators are 128 columns wide: [0,64) = hi.W_hi + lo.W_hi, [64,128) = hi.W_lo
+    // (one N=128 MMA reads A_hi once against [W_hi; W_lo], which are contiguous in smem)
+    static constexpr uint32_t C_D0 = 0, C_D1 = 256, C_A1 = 384, D0W = 128;
+    static constexpr uint32_t IDESC_N128 = tc::idesc(TM, 2 * H);
 
     static __device__ __forceinline__ uint64_t *bar(unsigned char *sm, int i) {
         return reinterpret_cast<uint64_t *>(sm + OFF_BAR) + i;
@@ -83,7 +87,7 @@ struct TcPipe {
         if (T == 0) return;
         // role timers (GMPGR_PHASE_TIMING): one writer thread per slot
         //   0 E layer-0 epilogue  1 E layer-1 epilogue  2 E d0full-wait  3 E d1full-wait  4 E total
-        //   5 issuer idle (polling, nothing ready)  7 loader empty-wait
+        //   5 issuer idle (polling, nothing ready)  6 issuer busy issuing MMAs  7 loader empty-wait
         const long long t_run = sub ? clock64() : 0;
 #define TP_WAIT(slot, expr)                                                   \
     do {                                                                      \
@@ -97,24 +101,29 @@ struct TcPipe {
             const int lt = tid - 32 * L_WARP0, lw = lt >> 5;
             constexpr int NLW = NL / 32, UPC = TM * 16 / 32, UPW = (UPC + NLW - 1) / NLW;
             const int rl = lane & 7, pl = lane >> 3;
-            int32_t nxt[UPW];  // slots of the next tile's rows (loaded one tile ahead)
-            auto load_slots = [&](int t) {
-                const int base = t * TM, nv = min(TM, n - base);
+            // slots of the rows of tiles t+1 and t+2: the slot loads are issued two tiles
+            // before their rows are gathered, so their latency never gates the cp.async issue
+            int32_t nx1[UPW], nx2[UPW];
+            auto load_slots = [&](int t, int32_t (&dst)[UPW]) {
+                const int base = t * TM, nv = t < T ? min(TM, n - base) : 0;
 #pragma unroll
                 for (int i = 0; i < UPW; ++i) {
                     const int un = lw + NLW * i, r = (un % (TM / 8)) * 8 + rl;
-                    nxt[i] = (un < UPC && r < nv) ? slots[base + r] : -1;
+                    dst[i] = (un < UPC && r < nv) ? slots[base + r] : -1;
                 }
             };
-            load_slots(0);
+            load_slots(0, nx1);
+            load_slots(1, nx2);
             for (int t = 0; t < T; ++t) {
                 const uint16_t *rp[UPW];
 #pragma unroll
                 for (int i = 0; i < UPW; ++i)
-                    rp[i] = nxt[i] >= 0 ? it.hl + (it.hl_by_slot ? (int64_t)nxt[i] : slot_row(g, nxt[i])) *
+                    rp[i] = nx1[i] >= 0 ? it.hl + (it.hl_by_slot ? (int64_t)nx1[i] : slot_row(g, nx1[i])) *
                                                       (2 * (int64_t)D_H)
                                         : nullptr;
-                if (t + 1 < T) load_slots(t + 1);
+#pragma unroll
+                for (int i = 0; i < UPW; ++i) nx1[i] = nx2[i];
+                load_slots(t + 2, nx2);
 #pragma unroll
                 for (int kc = 0; kc < NC; ++kc) {
                     const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, u = qg / S;
@@ -136,28 +145,36 @@ struct TcPipe {
                 }
             }
         } else if (warp == ISSUER_WARP) {
-            // ================= MMA issuer (one thread): polls the barriers and issues
-            // whatever is ready -- layer 1 of an earlier tile as soon as its A1 operand is in
-            // TMEM, else the next layer-0 K chunk -- so neither waits behind the other
-            if (lane == 0) {
-                const uint32_t bH0 = tc::smem_u32(sm + OFF_B0H), bL0 = tc::smem_u32(sm + OFF_B0L);
+            // ================= MMA issuer (one warp, converged; elect.sync issues): polls the
+            // barriers and issues whatever is ready -- layer 1 of an earlier tile as soon as
+            // its A1 operand is in TMEM, else the next layer-0 K chunk.  Barrier probes are
+            // made warp-uniform (lane 0's answer) so control flow never diverges.
+            {
+                constexpr unsigned FULLM = 0xffffffffu;
+                const uint32_t bH0 = tc::smem_u32(sm + OFF_B0H);
                 const uint32_t bH1 = tc::smem_u32(sm + OFF_B1H), bL1 = tc::smem_u32(sm + OFF_B1L);
+                auto ready = [&](int b, uint32_t par) {
+                    return __shfl_sync(FULLM, lane == 0 ? (int)tc::mbar_test(bar(sm, b), par) : 0, 0) != 0;
+                };
                 int l0t = 0, l0k = 0, l1t = 0;
                 long long idle0 = 0;
+                const bool tim = sub && lane == 0;
                 while (l1t < T) {
                     if (l1t < l0t) {
                         const uint32_t tg = tile_ctr + l1t, e = tg & 1u, v = tg >> 1;
-                        if (tc::mbar_test(bar(sm, A1FULL0 + e), v & 1u)) {
+                        if (ready(A1FULL0 + e, v & 1u)) {
+                            const long long ti0 = tim ? clock64() : 0;
                             tc::fence_after();
                             const uint32_t a1 = tmem + C_A1 + 64 * e, d1 = tmem + C_D1 + 64 * e;
 #pragma unroll
                             for (int k = 0; k < H / 16; ++k) {
                                 const uint64_t bh = tc::desc(bH1 + k * 256, H), bl = tc::desc(bL1 + k * 256, H);
-                                tc::mma_ts(d1, a1 + k * 8, bh, IDESC, k ? 1u : 0u);  // hi . hi
-                                tc::mma_ts(d1, a1 + k * 8, bl, IDESC, 1u);           // hi . lo
-                                tc::mma_ts(d1, a1 + 32 + k * 8, bh, IDESC, 1u);      // lo . hi
+                                tc::mma_ts_w(d1, a1 + k * 8, bh, IDESC, k ? 1u : 0u);  // hi . hi
+                                tc::mma_ts_w(d1, a1 + k * 8, bl, IDESC, 1u);           // hi . lo
+                                tc::mma_ts_w(d1, a1 + 32 + k * 8, bh, IDESC, 1u);      // lo . hi
                             }
-                            tc::commit(bar(sm, D1FULL0 + e));
+                            tc::commit_w(bar(sm, D1FULL0 + e));
+                            if (tim) sub[6] += (unsigned long long)(clock64() - ti0);
                             ++l1t;
                             idle0 = 0;
                             continue;
@@ -167,31 +184,31 @@ struct TcPipe {
                     if (l0t < T) {
                         const uint32_t tg = tile_ctr + l0t, e = tg & 1u, v = tg >> 1;
                         const uint32_t qg = chunk_ctr + l0t * NC + l0k, s = qg % S, u = qg / S;
-                        if ((l0k != 0 || v == 0 || tc::mbar_test(bar(sm, D0EMPTY0 + e), (v - 1) & 1u)) &&
-                            tc::mbar_test(bar(sm, FULL0 + s), u & 1u)) {
+                        if ((l0k != 0 || v == 0 || ready(D0EMPTY0 + e, (v - 1) & 1u)) && ready(FULL0 + s, u & 1u)) {
+                            const long long ti0 = tim ? clock64() : 0;
                             tc::fence_async_smem();
                             tc::fence_after();
-                            const uint32_t d0 = tmem + C_D0 + 64 * e;
+                            const uint32_t d0 = tmem + C_D0 + D0W * e;
                             const uint32_t aH = tc::smem_u32(sm + OFF_A + s * 2 * CH_BYTES), aL = aH + CH_BYTES;
 #pragma unroll
                             for (int k = 0; k < KC / 16; ++k) {
                                 const uint64_t ah = tc::desc(aH + k * 256, KC), al = tc::desc(aL + k * 256, KC);
                                 const uint32_t kb = (l0k * (KC / 16) + k) * 256;
-                                const uint64_t bh = tc::desc(bH0 + kb, D_H), bl = tc::desc(bL0 + kb, D_H);
-                                tc::mma(d0, ah, bh, IDESC, (l0k | k) ? 1u : 0u);
-                                tc::mma(d0, ah, bl, IDESC, 1u);
-                                tc::mma(d0, al, bh, IDESC, 1u);
+                                const uint64_t bh = tc::desc(bH0 + kb, D_H);
+                                tc::mma_w(d0, ah, bh, IDESC_N128, (l0k | k) ? 1u : 0u);  // hi . [W_hi; W_lo]
+                                tc::mma_w(d0, al, bh, IDESC, 1u);                          // lo . W_hi
                             }
-                            tc::commit(bar(sm, EMPTY0 + s));
+                            tc::commit_w(bar(sm, EMPTY0 + s));
+                            if (tim) sub[6] += (unsigned long long)(clock64() - ti0);
                             if (++l0k == NC) {
-                                tc::commit(bar(sm, D0FULL0 + e));
+                                tc::commit_w(bar(sm, D0FULL0 + e));
                                 l0k = 0;
                                 ++l0t;
                             }
                             issued = true;
                         }
                     }
-                    if (sub) {  // issuer idle time (no barrier ready)
+                    if (tim) {  // issuer idle time (no barrier ready)
                         const long long now = clock64();
                         if (!issued && idle0) sub[5] += (unsigned long long)(now - idle0);
                         idle0 = issued ? 0 : now;
@@ -223,11 +240,15 @@ struct TcPipe {
                 const long long te0 = timer ? clock64() : 0;
                 float h[64];
                 {
-                    float va[32], vb[32];
-                    tc::tmem_ld32(tmem + lanebase + C_D0 + 64 * e, va);
-                    tc::tmem_ld32(tmem + lanebase + C_D0 + 64 * e + 32, vb);
+                    const uint32_t d0 = tmem + lanebase + C_D0 + D0W * e;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) { h[j] = va[j]; h[32 + j] = vb[j]; }
+                    for (int half = 0; half < 2; ++half) {
+                        float va[32], vb[32];
+                        tc::tmem_ld32(d0 + 32 * half, va);
+                        tc::tmem_ld32(d0 + 64 + 32 * half, vb);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) h[32 * half + j] = va[j] + vb[j];
+                    }
                 }
                 tc::fence_before();
                 tc::mbar_arrive(bar(sm, D0EMPTY0 + e));
