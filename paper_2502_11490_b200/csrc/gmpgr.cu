@@ -826,14 +826,19 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     // order 237 ms (those variants were retired from the build).
     if (mode == GR_MODE_TC && I->di.hl == nullptr) return -1;
     const bool pipe = mode == GR_MODE_TC;
-    // tensor-core mode advances 16 queries per CTA (cfg3: 234.6 -> 221.5 ms vs 8), exact mode 8
-    int smem = 0, nthreads = 512, gq = pipe ? 16 : 8;
+    // tensor-core mode advances 16 queries per CTA (cfg3: 234.6 -> 221.5 ms vs 8) once the
+    // batch fills every SM twice over; smaller batches use 8 (more CTAs busy); exact mode 8
+    const bool g16 = pipe && Q >= 2 * 16 * (int64_t)num_sms(G->device);
+    int smem = 0, nthreads = 512, gq = g16 ? 16 : 8;
     void (*kern)(const SearchArgs) = nullptr;
 #define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \
     case CODE:                                                                                     \
-        if (pipe) {                                                                                \
+        if (g16) {                                                                                 \
             smem = plan_mq<DH, ZZ, 1, 512, 16, DH, true>(p->k, p->k_parallel, a);                  \
             kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 16, DH, true>;                                \
+        } else if (pipe) {                                                                         \
+            smem = plan_mq<DH, ZZ, 1, 512, 8, DH, true>(p->k, p->k_parallel, a);                   \
+            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH, true>;                                 \
         } else {                                                                                   \
             smem = plan_mq<DH, ZZ, 0, 512, 8, DH>(p->k, p->k_parallel, a);                         \
             kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH, false>;                                \

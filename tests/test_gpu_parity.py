@@ -259,3 +259,24 @@ def test_tc_first_pass_error_far_inside_refinement_band(P):
         worst = max(worst, float(np.max(np.abs(approx - exact) / band)))
     print(f"max |approx-exact| / band = {worst:.3e}")
     assert worst < 0.05
+
+
+@pytest.mark.parametrize("fixture", ["search_d64_z2", "search_d128_z3"])
+def test_tensor_core_mode_large_batch_matches_reference(P, fixture):
+    """Batches that fill every SM twice run 16 queries per CTA (launch_mq): the reference's
+    recorded results must come back for every copy of every query."""
+    z = G.load(fixture)
+    metric = metric_of(P, z)
+    index = index_of(P, z)
+    nq = len(z["users"])
+    reps = -(-5000 // nq)
+    users = np.tile(z["users"], (reps, 1))
+    pi, p = G.param_sets(z)[0]
+    r = P.c_hipanns_batch(index, metric, users, z["emb"], P.SearchParams(**p, mode="tc"))
+    exp = G.expected(z, pi)
+    for rep in range(reps):
+        sl = slice(rep * nq, (rep + 1) * nq)
+        np.testing.assert_array_equal(r.ids[sl], exp["ids"])
+        np.testing.assert_array_equal(r.scores[sl], exp["scores"])
+        np.testing.assert_array_equal(r.evals[sl], exp["evals"])
+        np.testing.assert_array_equal(r.hops_to_best[sl], exp["best_hop"])
