@@ -39,6 +39,24 @@ def log(*a):
     print(*a, file=sys.stderr, flush=True)
 
 
+# stdout carries exactly one JSON line: everything else the process (NCCL banners, library
+# prints) writes to file descriptor 1 is sent to stderr, the line goes to the saved stdout
+_JSON_OUT = None
+
+
+def _isolate_stdout():
+    global _JSON_OUT
+    sys.stdout.flush()
+    _JSON_OUT = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
+
+
+def emit(line: dict):
+    out = _JSON_OUT or sys.stdout
+    out.write(json.dumps(line) + "\n")
+    out.flush()
+
+
 def peaks():
     try:
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -194,7 +212,7 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
     if dist:
         dist.destroy_process_group()
     return 0
@@ -377,7 +395,7 @@ def run_gmpgr(args):
                                           f"relevance), {threads} threads, {t:.1f}s"}
         line["ids_identical_to_cpu_reference"] = float(same)
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -442,7 +460,7 @@ def run_sharded(args):
         "scoring_mode": args.mode,
     }
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.barrier()
         dist.destroy_process_group()
@@ -450,6 +468,7 @@ def run_sharded(args):
 
 
 def main():
+    _isolate_stdout()
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
