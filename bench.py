@@ -481,10 +481,15 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--k-parallel", type=int, default=PARAMS["k_parallel"],
+                    help="search budget override (default: the reference's evalharness defaults)")
+    ap.add_argument("--hops", type=int, default=PARAMS["hops"])
+    ap.add_argument("--ef", type=int, default=PARAMS["ef"])
     ap.add_argument("--mode", default="tc", choices=["exact", "tc"],
                     help="exact: CUDA-core exact-fp32 scoring; tc: tcgen05 split-bf16 scoring "
                          "with exact re-scoring of every near-threshold item")
     args = ap.parse_args()
+    PARAMS.update(k_parallel=args.k_parallel, hops=args.hops, ef=args.ef)
     if args.impl == "reference":
         return run_reference(args)
     if args.config == "cfg4":
