@@ -783,7 +783,7 @@ int plan_mq(int k, int kp, SearchArgs &a) {
         }
         a.off_acc0 = P.alloc(G * 64 * 16);
         a.off_kp = P.alloc(3 * G * kp * 4);
-        return P.bytes;
+        return P.bytes + 1024;  // slack for the kernel's 1024-byte alignment of the carve
     }
     a.off_w0 = NT >= 512 ? P.alloc(EX::W_END * 16) : 0;
     a.off_x0 = P.alloc(std::max(EX::BUF_END * 16, MODE == 1 ? TC::A_BYTES : 0));
@@ -809,6 +809,37 @@ int ensure_slot_hl(gr_graph *G, const gr_items *I, cudaStream_t stream) {
     GR_CUDA(cudaGetLastError());
     G->hl_serial = I->serial;
     return GR_OK;
+}
+
+// Tensor map over a bf16 hi/lo item table [rows][2d] for the TMA gather4 loader: 64-element
+// (128-byte) boxes of one row, 128-byte swizzle.  cuTensorMapEncodeTiled comes from the driver
+// through the runtime's entry-point query (no -lcuda link).
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+int make_hl_map(CUtensorMap *map, const uint16_t *hl, int64_t rows, int d) {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        GR_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+        if (!p || q != cudaDriverEntryPointSuccess) return fail(GR_ECUDA, "cuTensorMapEncodeTiled not available");
+        fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)(2 * d), (cuuint64_t)rows};
+    const cuuint64_t strides[1] = {(cuuint64_t)(2 * d) * 2};
+    const cuuint32_t box[2] = {64, 1}, estr[2] = {1, 1};
+    const CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<uint16_t *>(hl), dims, strides, box,
+                          estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail(GR_ECUDA, "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")");
+    return GR_OK;
+}
+
+bool env_flag(const char *name, bool dflt) {
+    const char *v = std::getenv(name);
+    if (!v || !*v) return dflt;
+    return v[0] != '0';
 }
 
 // multi-query kernel for the fixed model shapes (search_mq.cuh); returns -1 if not applicable
@@ -871,6 +902,11 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
         if (int rc = ensure_slot_hl(const_cast<gr_graph *>(G), I, stream)) return rc;
         a.it.hl = G->hl_slot;
         a.it.hl_by_slot = 1;
+    }
+    if (pipe && env_flag("GMPGR_TMA", true)) {  // GMPGR_TMA=0: cp.async loaders
+        const int64_t rows = a.it.hl_by_slot ? G->dg.n : I->di.n;
+        if (int rc = make_hl_map(&a.hl_map, a.it.hl, rows, I->di.d)) return rc;
+        a.tma = 1;
     }
     a.users = users;
     a.Q = Q;

@@ -18,6 +18,8 @@
 // A tag below epoch<<32 means "unclaimed in this query".  One atomic per
 // neighbour read; owners are resolved after a CTA barrier.
 #pragma once
+#include <cuda.h>
+
 #include "common.cuh"
 #include "mlp_exact.cuh"
 #include "select.cuh"
@@ -63,6 +65,10 @@ struct SearchArgs {
     const uint32_t *tab_code;
     const double *tab_f64;
     int64_t tab_n;
+    // tensor-core pipeline A-operand loader: TMA tile::gather4 over the bf16 hi/lo item table
+    // (GMPGR_TMA), else per-thread cp.async
+    int tma;
+    CUtensorMap hl_map;
 };
 
 struct CtaState {

@@ -362,7 +362,7 @@ struct MqState {
 // Shared-memory plan (host computes the same offsets): [model block][exact buffers]
 // [hist NW x 256][sort G x sortcap keys+vals][seg cnt/off/fn: 3 x G*kp][acc0 G x 64 float4]
 template <int DH, int ZZ, int MODE, int NT, int G, int KC, bool PIPE>
-__global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(const SearchArgs a) {
+__global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(const __grid_constant__ SearchArgs a) {
     constexpr int NW = NT / 32, GT = NT / G;
     // exact weight block in smem, else the global image (the pipelined scorer needs the room)
     constexpr bool W_SMEM = (NT >= 512) && !(MODE == 1 && PIPE);
@@ -377,7 +377,11 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
     constexpr int OFF_TMEMP = PIPE ? TP::OFF_TMEM : TC::OFF_TMEM;
     constexpr uint32_t TMEM_COLS = PIPE ? TP::TMEM_COLS : 128;
     uint32_t chunk_ctr = 0, tile_ctr = 0;  // pipelined scorer barrier phases
-    extern __shared__ __align__(16) unsigned char smem[];
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    // the pipelined scorer's SWIZZLE_128B A stages need 1024-byte aligned shared addresses; the
+    // dynamic window is not 1024-aligned next to the static state, so the host plan reserves
+    // 1024 bytes of slack (plan_mq) and the carve starts at the next 1024-byte boundary
+    unsigned char *const smem = PIPE ? smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
     __shared__ MqState<G> st;
     __shared__ unsigned long long ph_acc[16];
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -431,7 +435,11 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                              tc::smem_u32(tptr)), "r"(TMEM_COLS));
             asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
         }
-        if constexpr (PIPE) TP::init_barriers(tcs);
+        if constexpr (PIPE) {
+            // SWIZZLE_128B stages need 1024-byte aligned shared addresses
+            if (a.tma && (tc::smem_u32(tcs + TP::OFF_A) & 1023u)) __trap();
+            TP::init_barriers(tcs, a.tma != 0);
+        }
         else if (tid == 0) tc::mbar_init(reinterpret_cast<uint64_t *>(tcs + TC::OFF_BAR), 1);
         tc::fence_before();
         __syncthreads();
@@ -518,7 +526,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                                 pslot(gq, Q.pool_cur)[idx] = s;
                                 pmeta(gq, Q.pool_cur)[idx] = hop << 1;
                             }
-                        }, a.phase_cycles ? ph_acc + 8 : nullptr);
+                        }, a.phase_cycles ? ph_acc + 8 : nullptr, a.tma ? &a.hl_map : nullptr);
                 if (tid == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
                 __syncthreads();
             } else if constexpr (MODE == 1) {

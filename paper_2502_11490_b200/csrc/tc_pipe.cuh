@@ -28,6 +28,7 @@ template <int D_H, int Z, int G>
 struct TcPipe {
     static constexpr int H = 64, TM = 128, KC = 64, NC = D_H / KC, S = 4;
     static constexpr int NT = 512, NE = 128, ISSUER_WARP = 8, L_WARP0 = 9, NL = NT - 32 * L_WARP0;
+    static constexpr int NOPS = 2 * TM / 4;  // TMA gather4 ops per K chunk (hi + lo)
     // byte offsets
     static constexpr int OFF_B0H = 0;
     static constexpr int OFF_B0L = OFF_B0H + H * D_H * 2;
@@ -59,10 +60,10 @@ struct TcPipe {
         return reinterpret_cast<uint64_t *>(sm + OFF_BAR) + i;
     }
 
-    static __device__ void init_barriers(unsigned char *sm) {
+    static __device__ void init_barriers(unsigned char *sm, bool tma = false) {
         if (threadIdx.x == 0) {
             for (int s = 0; s < S; ++s) {
-                tc::mbar_init(bar(sm, FULL0 + s), NL);
+                tc::mbar_init(bar(sm, FULL0 + s), tma ? NOPS : NL);
                 tc::mbar_init(bar(sm, EMPTY0 + s), 1);
             }
             for (int e = 0; e < 2; ++e) {
@@ -81,10 +82,17 @@ struct TcPipe {
     static __device__ __forceinline__ void run(unsigned char *sm, uint32_t tmem, const DevItems &it,
                                                const DevGraph &g, const int32_t *slots, const int32_t *gis,
                                                int n, uint32_t &chunk_ctr, uint32_t &tile_ctr,
-                                               OnScore on_score, unsigned long long *sub = nullptr) {
+                                               OnScore on_score, unsigned long long *sub = nullptr,
+                                               const void *tmap = nullptr) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         const int T = (n + TM - 1) / TM;
         if (T == 0) return;
+        if (tmap) {
+            // the A stages alias generic-proxy buffers outside run(); order those accesses
+            // before the TMA (async-proxy) writes into them
+            tc::fence_async_smem();
+            __syncthreads();
+        }
         // role timers (GMPGR_PHASE_TIMING): one writer thread per slot
         //   0 E layer-0 epilogue  1 E layer-1 epilogue  2 E d0full-wait  3 E d1full-wait  4 E total
         //   5 issuer idle (polling, nothing ready)  6 issuer busy issuing MMAs  7 loader empty-wait
@@ -95,7 +103,44 @@ struct TcPipe {
         expr;                                                                 \
         if (sub) sub[slot] += (unsigned long long)(clock64() - w0_);          \
     } while (0)
-        if (warp >= L_WARP0) {
+        if (warp >= L_WARP0 && tmap) {
+            // ================= TMA loaders: per K chunk, 64 tile::gather4 ops (32 four-row groups x
+            // hi/lo halves, 128-byte swizzled rows = the SWIZZLE_128B K-major UMMA layout) spread
+            // over the 7 loader warps (<= 10 issuing lanes each); every issuing lane arms the
+            // stage's full barrier with its own 512 bytes (init count NOPS)
+            const int lw = warp - L_WARP0, o = lane * (NL / 32) + lw;
+            if (o < NOPS) {
+                const int grp = o >> 1, half = o & 1;
+                auto rows_of = [&](int t, int (&dst)[4]) {
+                    const int base = t * TM, nv = t < T ? min(TM, n - base) : 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = 4 * grp + j;
+                        const int32_t sl = r < nv ? slots[base + r] : -1;
+                        dst[j] = sl < 0 ? 0 : (it.hl_by_slot ? (int)sl : (int)slot_row(g, sl));
+                    }
+                };
+                int nx[4];
+                rows_of(0, nx);
+                for (int t = 0; t < T; ++t) {
+                    int cur[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) cur[j] = nx[j];
+                    if (t + 1 < T) rows_of(t + 1, nx);
+#pragma unroll
+                    for (int kc = 0; kc < NC; ++kc) {
+                        const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, u = qg / S;
+                        if (u >= 1) {
+                            if (sub && o == 0) TP_WAIT(7, tc::mbar_wait(bar(sm, EMPTY0 + s), (u - 1) & 1u));
+                            else tc::mbar_wait(bar(sm, EMPTY0 + s), (u - 1) & 1u);
+                        }
+                        tc::mbar_arrive_expect_tx(bar(sm, FULL0 + s), 512);
+                        tc::tma_gather4(tc::smem_u32(sm + OFF_A + s * 2 * CH_BYTES) + half * CH_BYTES + grp * 512, tmap,
+                                        half * D_H + kc * KC, cur[0], cur[1], cur[2], cur[3], bar(sm, FULL0 + s));
+                    }
+                }
+            }
+        } else if (warp >= L_WARP0) {
             // ================= loaders: unit = 8 rows x 4 pieces of 16 B (conflict-free
             // core-matrix stores); pieces 0-7 = hi k 0..63 of the chunk, 8-15 = lo
             const int lt = tid - 32 * L_WARP0, lw = lt >> 5;
@@ -192,7 +237,8 @@ struct TcPipe {
                             const uint32_t aH = tc::smem_u32(sm + OFF_A + s * 2 * CH_BYTES), aL = aH + CH_BYTES;
 #pragma unroll
                             for (int k = 0; k < KC / 16; ++k) {
-                                const uint64_t ah = tc::desc(aH + k * 256, KC), al = tc::desc(aL + k * 256, KC);
+                                const uint64_t ah = tmap ? tc::desc_sw128(aH + k * 32) : tc::desc(aH + k * 256, KC);
+                                const uint64_t al = tmap ? tc::desc_sw128(aL + k * 32) : tc::desc(aL + k * 256, KC);
                                 const uint32_t kb = (l0k * (KC / 16) + k) * 256;
                                 const uint64_t bh = tc::desc(bH0 + kb, D_H);
                                 tc::mma_w(d0, ah, bh, IDESC_N128, (l0k | k) ? 1u : 0u);  // hi . [W_hi; W_lo]

@@ -148,6 +148,32 @@ __device__ __forceinline__ void cp_async16(uint32_t sdst, const void *gsrc) {
 __device__ __forceinline__ void cp_async_arrive(uint64_t *bar) {
     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// TMA row gather: 4 rows x 64 bf16 (the tensor map's 128-byte box) of a 2-D [rows][cols] table
+// into 512 contiguous bytes of shared memory, 128-byte swizzled; completion counted in bytes
+// on the mbarrier (the issuer armed it with arrive.expect_tx)
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void tma_gather4(uint32_t sdst, const void *tmap, int col, int r0, int r1, int r2,
+                                            int r3, uint64_t *bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(sdst),
+        "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
+        : "memory");
+}
+// K-major SWIZZLE_128B operand: 128-byte rows (64 bf16 of K), 8-row atoms 1024 B apart (SBO);
+// the K step inside the atom advances the start address by 32 B per 16 elements
+__device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                               // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024u >> 4) << 32;                    // SBO: next 8-row atom
+    d |= (uint64_t)1 << 46;                               // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                               // layout: SWIZZLE_128B
+    return d;
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
     return *reinterpret_cast<const uint32_t *>(&h);
