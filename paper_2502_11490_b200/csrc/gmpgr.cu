@@ -906,7 +906,7 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     if (pipe && env_flag("GMPGR_TMA", true)) {  // GMPGR_TMA=0: cp.async loaders
         const int64_t rows = a.it.hl_by_slot ? G->dg.n : I->di.n;
         if (int rc = make_hl_map(&a.hl_map, a.it.hl, rows, I->di.d)) return rc;
-        a.tma = 1;
+        a.tma = env_flag("GMPGR_TMA_PF", false) ? 2 : 1;  // 2: + L2 prefetch of the next tile's rows
     }
     a.users = users;
     a.Q = Q;

@@ -526,7 +526,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                                 pslot(gq, Q.pool_cur)[idx] = s;
                                 pmeta(gq, Q.pool_cur)[idx] = hop << 1;
                             }
-                        }, a.phase_cycles ? ph_acc + 8 : nullptr, a.tma ? &a.hl_map : nullptr);
+                        }, a.phase_cycles ? ph_acc + 8 : nullptr, a.tma ? &a.hl_map : nullptr, a.tma == 2);
                 if (tid == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
                 __syncthreads();
             } else if constexpr (MODE == 1) {

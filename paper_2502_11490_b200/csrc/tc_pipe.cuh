@@ -83,7 +83,7 @@ struct TcPipe {
                                                const DevGraph &g, const int32_t *slots, const int32_t *gis,
                                                int n, uint32_t &chunk_ctr, uint32_t &tile_ctr,
                                                OnScore on_score, unsigned long long *sub = nullptr,
-                                               const void *tmap = nullptr) {
+                                               const void *tmap = nullptr, bool pf = false) {
         const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
         const int T = (n + TM - 1) / TM;
         if (T == 0) return;
@@ -126,7 +126,14 @@ struct TcPipe {
                     int cur[4];
 #pragma unroll
                     for (int j = 0; j < 4; ++j) cur[j] = nx[j];
-                    if (t + 1 < T) rows_of(t + 1, nx);
+                    if (t + 1 < T) {
+                        rows_of(t + 1, nx);
+                        // warm L2 with the next tile's rows while this tile's stages drain
+                        if (pf)
+#pragma unroll
+                            for (int kc = 0; kc < NC; ++kc)
+                                tc::tma_prefetch_gather4(tmap, half * D_H + kc * KC, nx[0], nx[1], nx[2], nx[3]);
+                    }
 #pragma unroll
                     for (int kc = 0; kc < NC; ++kc) {
                         const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, u = qg / S;

@@ -163,6 +163,11 @@ __device__ __forceinline__ void tma_gather4(uint32_t sdst, const void *tmap, int
         "l"(tmap), "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3), "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_prefetch_gather4(const void *tmap, int col, int r0, int r1, int r2, int r3) {
+    asm volatile("cp.async.bulk.prefetch.tensor.2d.L2.global.tile::gather4 [%0, {%1, %2, %3, %4, %5}];" ::"l"(tmap),
+                 "r"(col), "r"(r0), "r"(r1), "r"(r2), "r"(r3)
+                 : "memory");
+}
 // K-major SWIZZLE_128B operand: 128-byte rows (64 bf16 of K), 8-row atoms 1024 B apart (SBO);
 // the K step inside the atom advances the start address by 32 B per 16 elements
 __device__ __forceinline__ uint64_t desc_sw128(uint32_t saddr) {
