@@ -184,6 +184,22 @@ int gr_search_scores(gr_searcher *s, const gr_graph *g, const gr_scores *t,
                      const gr_search_params *p, int64_t *out_ids, double *out_scores,
                      int32_t *out_count, int64_t *out_stats, int on_device, void *stream);
 
+/* Sequential index construction, node-for-node identical to the reference's
+ * GraphIndex.insert (index.py:283-319: layer descent with ef=1, ef_construction beam
+ * search per layer (_chot.pyx:116-179), keep-M or heuristic _select (index.py:226-239),
+ * symmetric _connect with capacity re-selection (index.py:250-281)).  Host code (no GPU).
+ * Inserts slots [n0, n1) in order; the caller has stored vectors fp64 [cap][dim],
+ * ids int64 [cap] and levels int32 [cap] (drawn from the reference's level stream,
+ * index.py:196-209) for those slots.  nbrs[l]: int32 [cap][2m (l == 0) or m], cnts[l]:
+ * int32 [cap] for l < max_layers (the reference's _nbrs/_cnts arrays, index.py:78-79),
+ * stamps int64 [cap] (index.py:80), *stamp the last used stamp, *entry_slot / *top_level
+ * (-1 when empty) are updated in place. */
+#define GR_MAX_GRAPH_LAYERS 8
+int gr_hnsw_insert(int64_t n0, int64_t n1, int32_t dim, const double *vectors, const int64_t *ids,
+                   const int32_t *levels, int32_t m, int32_t ef_construction, int32_t max_layers,
+                   int select_heuristic, int32_t *const *nbrs, int32_t *const *cnts,
+                   int64_t *stamps, int64_t *stamp, int32_t *entry_slot, int32_t *top_level);
+
 #ifdef __cplusplus
 }
 #endif

@@ -32,6 +32,7 @@ EXPORTS = (
     "gr_brute_force", "gr_merge_topk",
     "gr_scores_create", "gr_scores_euclid", "gr_scores_read", "gr_scores_destroy",
     "gr_search_scores",
+    "gr_hnsw_insert",
 )
 
 
@@ -77,6 +78,8 @@ def _declare(lib):
         "gr_scores_read": (C.c_int, [vp, vp]),
         "gr_scores_destroy": (C.c_int, [vp]),
         "gr_search_scores": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
+        "gr_hnsw_insert": (C.c_int, [i64, i64, i32, vp, vp, vp, i32, i32, i32, C.c_int, vp, vp,
+                                     vp, vp, vp, vp]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -9,13 +9,16 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 LIB = os.path.join(HERE, "libgmpgr.so")
-SOURCES = ["gmpgr.cu"]
+SOURCES = ["gmpgr.cu", "hnsw_build.cpp"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17",
     "-Xcompiler", "-fPIC", "-shared", "-cudart", "static",
     "-Xptxas", "-v",
+    # host code (hnsw_build.cpp) must keep separately rounded mul/add like the reference's
+    # compiled Cython and numpy loops: no FMA contraction
+    "-Xcompiler", "-ffp-contract=off",
 ]
 
 
@@ -25,7 +28,7 @@ def _stale() -> bool:
     t = os.path.getmtime(LIB)
     import glob
 
-    deps = [os.path.join(CSRC, f) for f in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh"))
+    deps = [os.path.join(CSRC, f) for f in SOURCES] + glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(CSRC, "*.h"))
     deps.append(os.path.join(os.path.dirname(HERE), "include", "gmpgr.h"))
     return any(os.path.getmtime(p) > t for p in deps if os.path.exists(p))
 

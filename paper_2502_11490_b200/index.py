@@ -4,8 +4,11 @@ Mirror of ``nann.index.GraphIndex`` (/root/reference/pkg/src/nann/index.py:30-50
 the read side the hot path consumes: same storage (per-layer fixed-width int32 rows of
 cap 2m / m plus counts, index.py:67-85), same ``graph_view()`` (index.py:384-391), same
 NANN-IDX format (index.py:24-27, 397-508), same ``validate()`` invariants
-(index.py:325-358).  ``build`` uses the GPU producer (builder.py); incremental
-``insert``/stream admission (index.py:283-319, 511-592) is outside the hot path.
+(index.py:325-358).  ``build``/``insert`` default to the native exact restatement of the
+reference's sequential insert (csrc/hnsw_build.cpp, ``gr_hnsw_insert``): the graph is
+identical node for node to ``nann.GraphIndex.build``.  ``build(method="gpu")`` is the
+bulk GPU producer (builder.py) for catalogs the sequential build cannot reach in
+minutes (10M+).  Stream admission (index.py:511-592) is outside the hot path.
 """
 
 from __future__ import annotations
@@ -52,6 +55,9 @@ class GraphIndex:
         self._cnts = [np.empty(0, dtype=np.int32) for _ in range(max_layers)]
         self._slot_map = None
         self._dev = {}
+        self._stamps = np.empty(0, dtype=np.int64)
+        self._stamp = 0
+        self._level_rng = None
         # embedding row per slot; None = the item id (model_scorer convention, search.py:88).
         # Catalog shards set it to the local row while ids stay global.
         self.rows = None
@@ -139,8 +145,31 @@ class GraphIndex:
     def build(cls, vectors, ids=None, m: int = 16, ef_construction: int = 64,
               level_prob: float = 1.0 / 17.0, max_layers: int = 4, seed: int = 0,
               select_heuristic: bool = False, kernel_backend: str | None = None,
-              device=None) -> "GraphIndex":
-        """Index a batch of vectors with the GPU producer (builder.py)."""
+              device=None, method: str = "exact") -> "GraphIndex":
+        """Index a batch of vectors.
+
+        ``method="exact"`` (default): iterated :meth:`insert` through the native
+        restatement of the reference build (index.py:160-194) -- same graph as
+        ``nann.GraphIndex.build`` for the same arguments.  ``method="gpu"``: the bulk
+        GPU producer (builder.py; reference level draws and entry point, k-NN edges).
+        """
+        if method == "exact":
+            vec = np.ascontiguousarray(np.asarray(vectors), dtype=np.float64)
+            if vec.ndim != 2 or vec.shape[0] < 1:
+                raise InvalidArgumentError("vectors must be a nonempty (n, d) array")
+            n = vec.shape[0]
+            ids = np.arange(n, dtype=np.int64) if ids is None else np.asarray(ids, dtype=np.int64)
+            if len(ids) != n:
+                raise InvalidArgumentError("ids and vectors differ in length")
+            if len(np.unique(ids)) != len(ids):
+                raise InvalidArgumentError("duplicate item ids")
+            idx = cls(dim=vec.shape[1], m=m, ef_construction=ef_construction,
+                      level_prob=level_prob, max_layers=max_layers, seed=seed,
+                      select_heuristic=select_heuristic, kernel_backend=kernel_backend)
+            idx._insert_batch(ids, vec)
+            return idx
+        if method != "gpu":
+            raise InvalidArgumentError(f"unknown build method {method!r}")
         from .builder import build_layers
 
         vec = vectors if not isinstance(vectors, np.ndarray) else np.ascontiguousarray(
@@ -163,9 +192,74 @@ class GraphIndex:
         idx._level_draws = n
         return idx
 
-    def insert(self, item_id: int, vector) -> None:  # pragma: no cover - outside the hot path
-        raise InvalidArgumentError(
-            "incremental insert is not part of the device hot path; rebuild with GraphIndex.build")
+    # ---------------------------------------------------------------- exact insert
+    def _reserve(self, n: int) -> None:
+        """Grow the slot arrays (index.py:91-116; same doubling, zero fill)."""
+        cap = len(self._ids)
+        if n <= cap and len(self._stamps) >= cap:
+            return
+        cap = max(n, 2 * cap, 16)
+        k = self._n
+        def grow(a, shape, dtype):
+            new = np.zeros(shape, dtype=dtype)
+            new[:k] = a[:k]
+            return new
+        self._vectors = grow(self._vectors, (cap, self.dim), np.float64)
+        self._ids = grow(self._ids, cap, np.int64)
+        self._levels = grow(self._levels, cap, np.int32)
+        self._stamps = grow(self._stamps, cap, np.int64)
+        for l in range(self.max_layers):
+            self._nbrs[l] = grow(self._nbrs[l], (cap, self._deg_cap(l)), np.int32)
+            self._cnts[l] = grow(self._cnts[l], cap, np.int32)
+
+    def _draw_levels(self, count: int) -> np.ndarray:
+        """Next ``count`` levels of the persistent level stream (index.py:196-209): one
+        uniform per insert from default_rng(seed), replayed to ``_level_draws``."""
+        if self._level_rng is None:
+            self._level_rng = np.random.default_rng(self.seed)
+            if self._level_draws:
+                self._level_rng.random(self._level_draws)
+        u = self._level_rng.random(count)
+        self._level_draws += count
+        with np.errstate(divide="ignore"):
+            lv = np.log(u) / np.log(self.level_prob)
+        top = self.max_layers - 1
+        return np.where(u <= 0.0, top, np.minimum(np.trunc(lv), top)).astype(np.int32)
+
+    def _insert_batch(self, ids: np.ndarray, vectors: np.ndarray) -> None:
+        ids = np.asarray(ids, dtype=np.int64)
+        vectors = np.ascontiguousarray(vectors, dtype=np.float64).reshape(len(ids), self.dim)
+        if self._n:
+            present = self._slot_of
+            for i in ids:
+                if int(i) in present:
+                    raise InvalidArgumentError(f"item id {int(i)} already present")
+        n0, n1 = self._n, self._n + len(ids)
+        self._reserve(n1)
+        self._vectors[n0:n1] = vectors
+        self._ids[n0:n1] = ids
+        self._levels[n0:n1] = self._draw_levels(len(ids))
+        stamp = np.array([self._stamp], dtype=np.int64)
+        entry = np.array([self._entry_slot], dtype=np.int32)
+        top = np.array([self._top_level], dtype=np.int32)
+        _lib.check(_lib.lib().gr_hnsw_insert(
+            n0, n1, self.dim, _lib.ptr(self._vectors), _lib.ptr(self._ids), _lib.ptr(self._levels),
+            self.m, self.ef_construction, self.max_layers, int(bool(self.select_heuristic)),
+            _lib.ptr_array(self._nbrs), _lib.ptr_array(self._cnts), _lib.ptr(self._stamps),
+            _lib.ptr(stamp), _lib.ptr(entry), _lib.ptr(top)))
+        self._n = n1
+        self._stamp = int(stamp[0])
+        self._entry_slot, self._top_level = int(entry[0]), int(top[0])
+        if self._slot_map is not None:
+            self._slot_map.update((int(i), n0 + j) for j, i in enumerate(ids))
+        self._dev = {}
+
+    def insert(self, item_id: int, vector) -> None:
+        """Add one item (index.py:283-319), exact native restatement; invariants hold on return."""
+        vector = np.asarray(vector, dtype=np.float64)
+        if vector.shape != (self.dim,):
+            raise InvalidArgumentError(f"vector shape {vector.shape} != ({self.dim},)")
+        self._insert_batch(np.array([item_id], dtype=np.int64), vector[None, :])
 
     # ---------------------------------------------------------------- invariants
     def validate(self) -> None:
