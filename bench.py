@@ -410,7 +410,7 @@ def run_sharded(args):
 
     dist, rank, world, local = dist_setup(args.gpus)
     from paper_2502_11490_b200 import workload
-    from paper_2502_11490_b200.distributed import ShardedSearcher, gather_lists, merge_lists
+    from paper_2502_11490_b200.distributed import ShardedSearcher, gather_lists, merge_packed
     from paper_2502_11490_b200.search import SearchParams, brute_force_batch
 
     wl = workload.make_shard(rank, world, shard_n=args.shard_n, n_queries=args.queries,
@@ -442,8 +442,7 @@ def run_sharded(args):
     gi, gsc = brute_force_batch(wl.model, wl.users[:nrec], wl.items, 100, device=local)
     gi = torch.from_numpy(gi + rank * args.shard_n).to(f"cuda:{local}")
     gsc = torch.from_numpy(gsc).to(f"cuda:{local}")
-    ai, asc = gather_lists(gi, gsc)
-    gt, _, _ = merge_lists(ai, asc, 100)
+    gt, _, _ = merge_packed(gather_lists(gi, gsc), 100)
     got = out[0][:nrec].cpu().numpy()
     gt = gt.cpu().numpy()
     recall = float(np.mean([len(set(got[q]) & set(gt[q])) / 100.0 for q in range(nrec)]))

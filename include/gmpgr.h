@@ -43,7 +43,9 @@ enum {
     GR_EINVAL = 1,   /* bad argument / contract violation */
     GR_ENUMERIC = 2, /* non-finite metric output (metric.py:134-135) */
     GR_ECUDA = 3,    /* CUDA runtime failure */
-    GR_ENOMEM = 4    /* device allocation failure */
+    GR_ENOMEM = 4,   /* device allocation failure */
+    GR_EBAND = 5     /* tensor-core mode: an approximate score missed its exact value by more
+                        than half the refinement band (async calls; gr_search re-runs exact) */
 };
 
 #define GR_ABI_VERSION 1
@@ -115,7 +117,9 @@ int gr_score_pairs(const gr_model *m, const gr_items *it, const float *users, in
 int gr_score_items_approx(const gr_model *m, const gr_items *it, const float *user,
                           const int64_t *item_ids, int64_t n, double *out_scores);
 
-/* Scratch owner for gr_search (visited tags, frontiers, pools).  One per stream. */
+/* Scratch owner for gr_search (visited state, frontiers, pools).  Calls on one searcher are
+ * serialised (a mutex covers staging, scratch growth, launch and read-back; launches on
+ * different streams are ordered by an event), so host threads may share it. */
 int gr_searcher_create(int device, gr_searcher **out);
 int gr_searcher_destroy(gr_searcher *s);
 
@@ -132,12 +136,16 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
               void *stream);
 
 /* Same as gr_search but asynchronous on `stream` with device pointers only; the numeric
- * flag is accumulated in the searcher and returned by gr_searcher_status. */
+ * flag and the tensor-core band certificate are accumulated in the searcher and returned
+ * by gr_searcher_status (GR_ENUMERIC / GR_EBAND).  gr_search itself checks the
+ * certificate and, if any approximate score missed its exact value by more than half the
+ * band, searches the batch again in exact mode before returning. */
 int gr_search_async(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_items *it,
                     const float *users, int64_t Q, const gr_search_params *p, int64_t *out_ids,
                     double *out_scores, int32_t *out_count, int64_t *out_stats, void *stream);
 /* Synchronise `stream`, return GR_ENUMERIC if any async search saw a non-finite output
- * since the last call (and clear the flag), else GR_OK. */
+ * since the last call, GR_EBAND if a tensor-core band violation was seen (flags cleared),
+ * else GR_OK. */
 int gr_searcher_status(gr_searcher *s, void *stream);
 /* kernel launches issued by this searcher so far (evidence counter for bench.py) */
 int64_t gr_searcher_launches(const gr_searcher *s);
@@ -146,7 +154,9 @@ int64_t gr_searcher_launches(const gr_searcher *s);
  * GMPGR_PHASE_TIMING=1 in the environment, out[2..9] = summed SM cycles per search phase
  * (init, seeds, expand, resolve, score, pool, frontier, output) and out[10..14] = cycles
  * inside tensor-core tiles (gather, layer-0 MMA wait, epilogue 0, layer-1 MMA wait,
- * epilogue 1).  out must hold 18 values.
+ * epilogue 1); out[18] = band violations seen (exact re-scores whose approximate score was
+ * farther than band/2 from the exact one), out[19] = largest |approx - exact| / band seen,
+ * as f32 bits, out[20] = batches gr_search re-ran in exact mode.  out must hold 22 values.
  * Synchronises the device. */
 int gr_searcher_counters(gr_searcher *s, int64_t *out);
 
@@ -161,6 +171,15 @@ int gr_brute_force(const gr_model *m, const gr_items *it, const float *users, in
 int gr_merge_topk(int device, const int64_t *in_ids, const double *in_scores, int32_t R,
                   int64_t Q, int32_t k_in, int32_t k, int64_t *out_ids, double *out_scores,
                   int32_t *out_count, void *stream);
+/* Shard-merge wire format, 8 bytes per entry (one all-gather instead of id + score
+ * gathers): gr_pack_topk packs n (id, score) entries as orderable(fp32 score) << 32 | id
+ * (requires 0 <= id < 2^32; id -1 -> 0 = empty); gr_merge_topk_packed merges R packed
+ * lists [R, Q, k_in] like gr_merge_topk.  Device pointers, asynchronous. */
+int gr_pack_topk(int device, const int64_t *ids, const double *scores, int64_t n, uint64_t *out,
+                 void *stream);
+int gr_merge_topk_packed(int device, const uint64_t *in, int32_t R, int64_t Q, int32_t k_in,
+                         int32_t k, int64_t *out_ids, double *out_scores, int32_t *out_count,
+                         void *stream);
 
 /* Traversal-only scorers (the reference's search tests: search.py:73-81 euclidean_scorer and
  * ad-hoc ScoreFns).  A score table holds fp64 scores [Q, n_items] indexed by ITEM ID (ids are

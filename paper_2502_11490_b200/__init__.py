@@ -18,6 +18,7 @@ from .batching import (
     run_dispatcher,
 )
 from .errors import (
+    BandError,
     DeviceError,
     FileFormatError,
     InvalidArgumentError,
@@ -61,7 +62,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "BatchClient", "BatchEngine", "BatchQueue", "BatchSearchResult", "DispatchStats", "Dispatcher",
-    "EvalRequest", "ModelBatchEngine", "run_dispatcher", "CandidatePool", "DeviceError", "FileFormatError",
+    "EvalRequest", "ModelBatchEngine", "run_dispatcher", "CandidatePool", "BandError", "DeviceError", "FileFormatError",
     "GpuBatchEngine", "GraphIndex", "InvalidArgumentError", "MetricModel", "NannError",
     "NumericError", "Projector", "QueueShutdownError", "RelevanceModel", "SearchParams",
     "SearchResult", "SearchStats", "WeightOverflowError", "brute_force", "brute_force_batch",

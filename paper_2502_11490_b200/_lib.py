@@ -12,12 +12,12 @@ import threading
 
 import numpy as np
 
-from .errors import DeviceError, InvalidArgumentError, NumericError
+from .errors import BandError, DeviceError, InvalidArgumentError, NumericError
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("GMPGR_LIB") or os.path.join(HERE, "libgmpgr.so")
 
-GR_OK, GR_EINVAL, GR_ENUMERIC, GR_ECUDA, GR_ENOMEM = 0, 1, 2, 3, 4
+GR_OK, GR_EINVAL, GR_ENUMERIC, GR_ECUDA, GR_ENOMEM, GR_EBAND = 0, 1, 2, 3, 4, 5
 
 # every symbol include/gmpgr.h declares (checked by tests/test_abi.py)
 EXPORTS = (
@@ -32,7 +32,7 @@ EXPORTS = (
     "gr_brute_force", "gr_merge_topk",
     "gr_scores_create", "gr_scores_euclid", "gr_scores_read", "gr_scores_destroy",
     "gr_search_scores",
-    "gr_hnsw_insert",
+    "gr_hnsw_insert", "gr_pack_topk", "gr_merge_topk_packed",
 )
 
 
@@ -78,6 +78,8 @@ def _declare(lib):
         "gr_scores_read": (C.c_int, [vp, vp]),
         "gr_scores_destroy": (C.c_int, [vp]),
         "gr_search_scores": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, vp]),
+        "gr_pack_topk": (C.c_int, [C.c_int, vp, vp, i64, vp, vp]),
+        "gr_merge_topk_packed": (C.c_int, [C.c_int, vp, i32, i64, i32, i32, vp, vp, vp, vp]),
         "gr_hnsw_insert": (C.c_int, [i64, i64, i32, vp, vp, vp, i32, i32, i32, C.c_int, vp, vp,
                                      vp, vp, vp, vp]),
     }
@@ -111,6 +113,8 @@ def check(rc: int):
         raise InvalidArgumentError(msg)
     if rc == GR_ENUMERIC:
         raise NumericError(msg)
+    if rc == GR_EBAND:
+        raise BandError(msg)
     if rc == GR_ENOMEM:
         raise MemoryError(msg)
     raise DeviceError(msg)
@@ -271,9 +275,12 @@ class DeviceSearcher(_Handle):
         return int(lib().gr_searcher_launches(self.h))
 
     def counters(self) -> dict:
-        out = np.zeros(18, dtype=np.int64)
+        out = np.zeros(22, dtype=np.int64)
         check(lib().gr_searcher_counters(self.h, ptr(out)))
-        d = {"exact_rescored": int(out[0]), "tensor_scored": int(out[1])}
+        d = {"exact_rescored": int(out[0]), "tensor_scored": int(out[1]),
+             "band_violations": int(out[18]),
+             "max_err_over_band": float(np.array([out[19]], dtype=np.uint32).view(np.float32)[0]),
+             "exact_reruns": int(out[20])}
         if out[2:10].any():
             names = ("init", "seeds", "expand", "resolve", "score", "pool", "frontier", "output")
             tot = float(out[2:10].sum())

@@ -342,3 +342,51 @@ __global__ void __launch_bounds__(GR_NT) merge_topk_kernel(const int64_t *in_ids
     }
     if (threadIdx.x == 0) out_count[q] = nr;
 }
+
+// ---------------------------------------------------------------------------
+// Shard-merge wire format (8 bytes per entry, one all-gather): orderable(fp32 score) << 32 |
+// id (0 <= id < 2^32); 0 = empty slot.  The returned scores are exact fp32 values widened to
+// fp64 (search.py:88), so the fp32 field is lossless.
+// ---------------------------------------------------------------------------
+__global__ void pack_topk_kernel(const int64_t *ids, const double *scores, int64_t n, uint64_t *out) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t id = ids[i];
+        out[i] = id < 0 ? 0ull : (((uint64_t)f32_orderable((float)scores[i]) << 32) | (uint64_t)(uint32_t)id);
+    }
+}
+
+// R packed lists per query -> one top-k by (score desc, id asc); one CTA per query
+__global__ void __launch_bounds__(GR_NT) merge_packed_kernel(const uint64_t *in, int R, int64_t Q, int kin,
+                                                             int k, int sortcap, int64_t *out_ids,
+                                                             double *out_scores, int32_t *out_count) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t *sk = reinterpret_cast<uint64_t *>(smem);
+    int32_t *sv = reinterpret_cast<int32_t *>(smem + sizeof(uint64_t) * sortcap);
+    __shared__ int total;
+    const int64_t q = blockIdx.x;
+    if (threadIdx.x == 0) total = 0;
+    __syncthreads();
+    for (int t = threadIdx.x; t < R * kin; t += GR_NT) {
+        const int r = t / kin, j = t % kin;
+        const uint64_t e = in[((int64_t)r * Q + q) * kin + j];
+        if (e) {
+            const int pos = atomicAdd(&total, 1);
+            sk[pos] = (e & 0xFFFFFFFF00000000ull) | (uint64_t)(~(uint32_t)e);
+            sv[pos] = (int32_t)(uint32_t)e;
+        }
+    }
+    __syncthreads();
+    const int n = total;
+    cta_sort_desc(sk, sv, n, sortcap);
+    const int nr = min(n, k);
+    for (int j = threadIdx.x; j < k; j += GR_NT) {
+        if (j < nr) {
+            out_ids[q * k + j] = (int64_t)(uint32_t)sv[j];
+            out_scores[q * k + j] = (double)orderable_f32((uint32_t)(sk[j] >> 32));
+        } else {
+            out_ids[q * k + j] = -1;
+            out_scores[q * k + j] = __longlong_as_double(0x7ff8000000000000ll);
+        }
+    }
+    if (threadIdx.x == 0) out_count[q] = nr;
+}

@@ -114,10 +114,16 @@ struct gr_graph {
     DevGraph dg;
     std::vector<void *> bufs;
     int max_deg;
+    int64_t max_row = 0;  // largest embedding row any slot reads (checked against the items)
     // bf16 hi/lo item rows in device-slot order for one items handle (built on first use),
-    // so the scorer's gathers follow the graph's locality and need no row indirection
+    // so the scorer's gathers follow the graph's locality and need no row indirection.
+    // hl_mu is held from the (re)build check until the search using it is enqueued, so a
+    // rebuild for another items handle (which synchronises the device first) never
+    // overwrites rows a queued search still reads.
     std::mutex hl_mu;
     uint64_t hl_serial = 0;
+    int64_t hl_n = 0;
+    int hl_d = 0;
     uint16_t *hl_slot = nullptr;
 };
 
@@ -165,6 +171,12 @@ struct gr_scores {
 
 struct gr_searcher {
     int device;
+    // one search at a time per searcher: staging buffers, scratch and the status flags are
+    // per searcher (ctypes releases the GIL, so Python threads can share one)
+    std::mutex mu;
+    // scratch reuse across streams: every launch waits for the previous one on this event
+    cudaEvent_t done = nullptr;
+    int64_t band_reruns = 0;
     int64_t slots = 0, n = 0, capF = 0, capS = 0, capP = 0;
     uint32_t *tags = nullptr;
     uint32_t *epochs = nullptr;
@@ -172,9 +184,9 @@ struct gr_searcher {
             *fr_v = nullptr, *fr_i = nullptr, *seg_v = nullptr, *pool_slot = nullptr;
     uint64_t *fr_key = nullptr, *seg_key = nullptr, *pool_key = nullptr;
     int32_t *pool_meta = nullptr;
-    unsigned long long *counters = nullptr;
+    unsigned long long *counters = nullptr; // [4]: see SearchArgs::counters
     unsigned long long *phase = nullptr; // [8] when GMPGR_PHASE_TIMING=1
-    int *flags = nullptr; // [0] queue, [1] nonfinite, [2] bad index
+    int *flags = nullptr; // [0] queue, [1] nonfinite, [2] bad index, [3] band violations
     int64_t launches = 0;
     // staging for host-pointer calls
     DevBuf st_users, st_ids, st_scores, st_count, st_stats;
@@ -462,6 +474,7 @@ int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *n
                 return cleanup(fail(GR_EINVAL, "item ids must be row indexes >= 0 (search.py:84-90)"));
             r[s] = (int32_t)v;
             ident &= (v == s);
+            G->max_row = std::max<int64_t>(G->max_row, v);
         }
         if (!ident) {
             int32_t *d = nullptr;
@@ -796,12 +809,20 @@ int plan_mq(int k, int kp, SearchArgs &a) {
     return P.bytes;
 }
 
+// Caller holds G->hl_mu until its search is enqueued.
 int ensure_slot_hl(gr_graph *G, const gr_items *I, cudaStream_t stream) {
-    std::lock_guard<std::mutex> lk(G->hl_mu);
     if (G->hl_slot && G->hl_serial == I->serial) return GR_OK;
-    if (I->di.n < G->dg.n) return fail(GR_EINVAL, "items table smaller than the graph");
+    if (G->max_row >= I->di.n) return fail(GR_EINVAL, "items table smaller than the graph");
+    // searches queued on any stream may still read the current copy
+    GR_CUDA(cudaDeviceSynchronize());
+    if (G->hl_slot && (G->hl_n != G->dg.n || G->hl_d != I->di.d)) {
+        cudaFree(G->hl_slot);
+        G->hl_slot = nullptr;
+    }
     if (!G->hl_slot) {
         if (int rc = dmalloc(&G->hl_slot, (size_t)G->dg.n * 2 * I->di.d)) return rc;
+        G->hl_n = G->dg.n;
+        G->hl_d = I->di.d;
     }
     const int64_t work = G->dg.n * (2 * I->di.d / 8);
     gather_hl_kernel<<<(unsigned)std::min<int64_t>((work + 255) / 256, 148 * 64), 256, 0, stream>>>(
@@ -859,7 +880,14 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     const bool pipe = mode == GR_MODE_TC;
     // tensor-core mode advances 16 queries per CTA (cfg3: 234.6 -> 221.5 ms vs 8) once the
     // batch fills every SM twice over; smaller batches use 8 (more CTAs busy); exact mode 8
-    const bool g16 = pipe && Q >= 2 * 16 * (int64_t)num_sms(G->device);
+    // re-score requests pack (query slot << 24 | index) with index < capS * G (CTA-level
+    // segment arrays) or < capP (per-query pools): larger budgets take the per-query kernel
+    const int64_t capS_q = std::max<int64_t>(std::min<int64_t>((int64_t)p->k_parallel * p->ef * G->max_deg,
+                                                               (int64_t)p->k_parallel * G->dg.n),
+                                             G->max_deg + 1) + 64;
+    const int64_t capP_q = p->k + capS_q;
+    if (capS_q * 8 >= (1 << 24) || capP_q >= (1 << 24)) return -1;
+    const bool g16 = pipe && Q >= 2 * 16 * (int64_t)num_sms(G->device) && capS_q * 16 < (1 << 24);
     int smem = 0, nthreads = 512, gq = g16 ? 16 : 8;
     void (*kern)(const SearchArgs) = nullptr;
 #define GR_MQ_CASE(CODE, DH, ZZ)                                                                   \
@@ -891,14 +919,14 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     if (per_sm < 1) return -1;
     const int64_t blocks = std::min<int64_t>((Q + G_ - 1) / G_, (int64_t)per_sm * num_sms(G->device));
     const int64_t capF = (int64_t)p->k_parallel * p->ef;
-    int64_t capS = std::min<int64_t>(capF * G->max_deg, (int64_t)p->k_parallel * G->dg.n);
-    capS = std::max<int64_t>(capS, G->max_deg + 1) + 64;
-    const int64_t capP = p->k + capS;
+    const int64_t capS = capS_q, capP = capP_q;
     if (int rc = ensure_search_scratch(S, G, blocks * G_, capF, capS, capP)) return rc;
     a.g = G->dg;
     a.M = M->dm;
     a.it = I->di;
+    std::unique_lock<std::mutex> hl_lock;
     if (pipe && mode == GR_MODE_TC && G->dg.rows) {
+        hl_lock = std::unique_lock<std::mutex>(const_cast<gr_graph *>(G)->hl_mu);
         if (int rc = ensure_slot_hl(const_cast<gr_graph *>(G), I, stream)) return rc;
         a.it.hl = G->hl_slot;
         a.it.hl_by_slot = 1;
@@ -941,6 +969,7 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     a.capP = S->capP;          // per-query pools
     a.queue = S->flags;
     a.nonfinite = S->flags + 1;
+    a.band_viol = S->flags + 3;
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
     kern<<<(int)blocks, nthreads, smem, stream>>>(a);
     GR_CUDA(cudaGetLastError());
@@ -1004,6 +1033,9 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
                   const float *users, int64_t Q, const gr_search_params *p, int64_t *ids,
                   double *scores, int32_t *count, int64_t *stats, cudaStream_t stream) {
     if (M->dm.d_h != I->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
+    if (G->max_row >= I->di.n)
+        return fail(GR_EINVAL, "graph reads embedding row " + std::to_string(G->max_row) + " but the items table has " +
+                                   std::to_string(I->di.n) + " rows (item_embeddings[ids], search.py:88)");
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
     const int shape = fixed_shape(M->dm);
@@ -1082,6 +1114,7 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     a.capP = S->capP;
     a.queue = S->flags;
     a.nonfinite = S->flags + 1;
+    a.band_viol = S->flags + 3;
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
     kern<<<(int)slots, GR_NT, smem, stream>>>(a);
     GR_CUDA(cudaGetLastError());
@@ -1167,8 +1200,15 @@ int gr_searcher_create(int device, gr_searcher **out) {
     S->device = device;
     if (int rc = dmalloc(&S->flags, 4)) { delete S; return rc; }
     cudaMemset(S->flags, 0, 16);
-    if (int rc = dmalloc(&S->counters, 2)) { cudaFree(S->flags); delete S; return rc; }
-    cudaMemset(S->counters, 0, 16);
+    if (int rc = dmalloc(&S->counters, 4)) { cudaFree(S->flags); delete S; return rc; }
+    cudaMemset(S->counters, 0, 32);
+    if (cudaEventCreateWithFlags(&S->done, cudaEventDisableTiming) != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(S->flags);
+        cudaFree(S->counters);
+        delete S;
+        return fail(GR_ECUDA, "cudaEventCreate failed");
+    }
     const char *pt = getenv("GMPGR_PHASE_TIMING");
     if (pt && pt[0] == '1') {
         if (dmalloc(&S->phase, 16) == GR_OK) cudaMemset(S->phase, 0, 128);
@@ -1180,9 +1220,14 @@ int gr_searcher_create(int device, gr_searcher **out) {
 int gr_searcher_destroy(gr_searcher *s) {
     if (!s) return GR_OK;
     cudaSetDevice(s->device);
+    {
+        std::lock_guard<std::mutex> lk(s->mu);
+        cudaDeviceSynchronize();
+    }
     s->free_scratch();
     cudaFree(s->flags);
     cudaFree(s->counters);
+    if (s->done) cudaEventDestroy(s->done);
     if (s->phase) cudaFree(s->phase);
     s->st_users.release();
     s->st_ids.release();
@@ -1197,10 +1242,18 @@ int64_t gr_searcher_launches(const gr_searcher *s) { return s ? s->launches : 0;
 
 int gr_searcher_counters(gr_searcher *s, int64_t *out) {
     if (!s || !out) return fail(GR_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
     GR_CUDA(cudaSetDevice(s->device));
     GR_CUDA(cudaDeviceSynchronize());
-    GR_CUDA(cudaMemcpy(out, s->counters, 16, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < 22; ++i) out[i] = 0;
+    uint64_t c[4];
+    GR_CUDA(cudaMemcpy(c, s->counters, 32, cudaMemcpyDeviceToHost));
+    out[0] = (int64_t)c[0];
+    out[1] = (int64_t)c[1];
     if (s->phase) GR_CUDA(cudaMemcpy(out + 2, s->phase, 128, cudaMemcpyDeviceToHost));
+    out[18] = (int64_t)c[2];
+    out[19] = (int64_t)c[3];
+    out[20] = s->band_reruns;
     return GR_OK;
 }
 
@@ -1211,22 +1264,40 @@ int gr_search_async(gr_searcher *s, const gr_graph *g, const gr_model *m, const 
         return fail(GR_EINVAL, "null argument");
     if (int rc = check_params(p)) return rc;
     if (Q <= 0) return GR_OK;
+    std::lock_guard<std::mutex> lk(s->mu);
     GR_CUDA(cudaSetDevice(s->device));
-    return launch_search(s, g, m, it, users, Q, p, out_ids, out_scores, out_count, out_stats,
-                         (cudaStream_t)stream);
+    cudaStream_t st = (cudaStream_t)stream;
+    GR_CUDA(cudaStreamWaitEvent(st, s->done, 0));
+    const int rc = launch_search(s, g, m, it, users, Q, p, out_ids, out_scores, out_count, out_stats, st);
+    GR_CUDA(cudaEventRecord(s->done, st));
+    return rc;
 }
+
+namespace {
+// flags[1] (non-finite) and flags[3] (tensor-core band violations) since the last read
+int read_status(gr_searcher *s, cudaStream_t st, int *nonfinite, int *band) {
+    GR_CUDA(cudaStreamWaitEvent(st, s->done, 0));
+    int f[4] = {0, 0, 0, 0};
+    GR_CUDA(cudaMemcpyAsync(f, s->flags, sizeof(f), cudaMemcpyDeviceToHost, st));
+    GR_CUDA(cudaStreamSynchronize(st));
+    if (f[1]) GR_CUDA(cudaMemsetAsync(s->flags + 1, 0, sizeof(int), st));
+    if (f[3]) GR_CUDA(cudaMemsetAsync(s->flags + 3, 0, sizeof(int), st));
+    *nonfinite = f[1];
+    *band = f[3];
+    return GR_OK;
+}
+}  // namespace
 
 int gr_searcher_status(gr_searcher *s, void *stream) {
     if (!s) return fail(GR_EINVAL, "null argument");
+    std::lock_guard<std::mutex> lk(s->mu);
     GR_CUDA(cudaSetDevice(s->device));
-    int flag = 0;
-    GR_CUDA(cudaMemcpyAsync(&flag, s->flags + 1, sizeof(int), cudaMemcpyDeviceToHost,
-                            (cudaStream_t)stream));
-    GR_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
-    if (flag) {
-        GR_CUDA(cudaMemsetAsync(s->flags + 1, 0, sizeof(int), (cudaStream_t)stream));
-        return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
-    }
+    int nonfinite = 0, band = 0;
+    if (int rc = read_status(s, (cudaStream_t)stream, &nonfinite, &band)) return rc;
+    if (nonfinite) return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
+    if (band)
+        return fail(GR_EBAND, std::to_string(band) + " tensor-core scores were farther than half the "
+                              "refinement band from their exact value: re-run in exact mode");
     return GR_OK;
 }
 
@@ -1238,12 +1309,16 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
         return fail(GR_EINVAL, "null argument");
     if (int rc = check_params(p)) return rc;
     if (Q <= 0) return GR_OK;
+    std::lock_guard<std::mutex> lk(s->mu);
     GR_CUDA(cudaSetDevice(s->device));
     cudaStream_t st = (cudaStream_t)stream;
-    GR_CUDA(cudaMemsetAsync(s->flags + 1, 0, sizeof(int), st));
+    GR_CUDA(cudaStreamWaitEvent(st, s->done, 0));
+    GR_CUDA(cudaMemsetAsync(s->flags + 1, 0, 3 * sizeof(int), st));
     const int nst = 5 + g->dg.n_layers;
+    gr_search_params pe = *p;
+    for (int attempt = 0;; ++attempt) {
     if (on_device) {
-        if (int rc = launch_search(s, g, m, it, users, Q, p, out_ids, out_scores, out_count,
+        if (int rc = launch_search(s, g, m, it, users, Q, &pe, out_ids, out_scores, out_count,
                                    out_stats, st))
             return rc;
     } else {
@@ -1263,8 +1338,8 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
         if (int rc = stage<int64_t>(s->st_stats, cap_s, ns)) return rc;
         s->st_stats_n = cap_s;
         float *du = (float *)s->st_users.p;
-        GR_CUDA(cudaMemcpyAsync(du, users, nu * 4, cudaMemcpyHostToDevice, st));
-        if (int rc = launch_search(s, g, m, it, du, Q, p, (int64_t *)s->st_ids.p,
+        if (attempt == 0) GR_CUDA(cudaMemcpyAsync(du, users, nu * 4, cudaMemcpyHostToDevice, st));
+        if (int rc = launch_search(s, g, m, it, du, Q, &pe, (int64_t *)s->st_ids.p,
                                    (double *)s->st_scores.p, (int32_t *)s->st_count.p,
                                    (int64_t *)s->st_stats.p, st))
             return rc;
@@ -1273,7 +1348,19 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
         GR_CUDA(cudaMemcpyAsync(out_count, s->st_count.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, st));
         GR_CUDA(cudaMemcpyAsync(out_stats, s->st_stats.p, ns * 8, cudaMemcpyDeviceToHost, st));
     }
-    return gr_searcher_status(s, stream);
+    GR_CUDA(cudaEventRecord(s->done, st));
+    int nonfinite = 0, band = 0;
+    if (int rc = read_status(s, st, &nonfinite, &band)) return rc;
+    if (nonfinite) return fail(GR_ENUMERIC, "non-finite value in metric forward pass");
+    // tensor-core certificate failed somewhere in the batch: the whole batch is searched
+    // again with exact scoring (results are then exact by construction)
+    if (band && pe.mode == GR_MODE_TC && attempt == 0) {
+        pe.mode = GR_MODE_EXACT;
+        s->band_reruns += 1;
+        continue;
+    }
+    return GR_OK;
+    }
 }
 
 // ------------------------------------------------------------------ score tables
@@ -1371,6 +1458,7 @@ int gr_search_scores(gr_searcher *s, const gr_graph *g, const gr_scores *t,
     if (int rc = check_params(p)) return rc;
     if (p->mode != GR_MODE_EXACT) return fail(GR_EINVAL, "score tables are exact-mode only");
     if (t->device != s->device || g->device != s->device) return fail(GR_EINVAL, "handles on different devices");
+    std::lock_guard<std::mutex> lk(s->mu);
     GR_CUDA(cudaSetDevice(s->device));
     {   // every item id must index the table (ids = score-table columns, search.py:79)
         std::vector<int64_t> hid(g->dg.n);
@@ -1380,8 +1468,12 @@ int gr_search_scores(gr_searcher *s, const gr_graph *g, const gr_scores *t,
     }
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t Q = t->Q, no = Q * p->k, ns = Q * (5 + g->dg.n_layers);
-    if (on_device)
-        return launch_search_scores(s, g, t, p, out_ids, out_scores, out_count, out_stats, st);
+    GR_CUDA(cudaStreamWaitEvent(st, s->done, 0));
+    if (on_device) {
+        const int rc = launch_search_scores(s, g, t, p, out_ids, out_scores, out_count, out_stats, st);
+        GR_CUDA(cudaEventRecord(s->done, st));
+        return rc;
+    }
     int64_t *di = nullptr, *dst = nullptr;
     double *ds = nullptr;
     int32_t *dc = nullptr;
@@ -1390,6 +1482,7 @@ int gr_search_scores(gr_searcher *s, const gr_graph *g, const gr_scores *t,
     if (!rc) rc = dmalloc(&dc, (size_t)Q);
     if (!rc) rc = dmalloc(&dst, (size_t)ns);
     if (!rc) rc = launch_search_scores(s, g, t, p, di, ds, dc, dst, st);
+    cudaEventRecord(s->done, st);
     if (!rc) {
         cudaMemcpyAsync(out_ids, di, no * 8, cudaMemcpyDeviceToHost, st);
         cudaMemcpyAsync(out_scores, ds, no * 8, cudaMemcpyDeviceToHost, st);
@@ -1619,6 +1712,33 @@ int gr_merge_topk(int device, const int64_t *in_ids, const double *in_scores, in
     if (int rc = set_smem(merge_topk_kernel, smem)) return rc;
     merge_topk_kernel<<<(unsigned)Q, GR_NT, smem, (cudaStream_t)stream>>>(
         in_ids, in_scores, R, Q, k_in, k, sortcap, out_ids, out_scores, out_count);
+    GR_CUDA(cudaGetLastError());
+    return GR_OK;
+}
+
+int gr_pack_topk(int device, const int64_t *ids, const double *scores, int64_t n, uint64_t *out,
+                 void *stream) {
+    if (!ids || !scores || !out) return fail(GR_EINVAL, "null argument");
+    if (n <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(device));
+    pack_topk_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 16), 256, 0, (cudaStream_t)stream>>>(
+        ids, scores, n, out);
+    GR_CUDA(cudaGetLastError());
+    return GR_OK;
+}
+
+int gr_merge_topk_packed(int device, const uint64_t *in, int32_t R, int64_t Q, int32_t k_in, int32_t k,
+                         int64_t *out_ids, double *out_scores, int32_t *out_count, void *stream) {
+    if (!in || !out_ids || !out_scores || !out_count) return fail(GR_EINVAL, "null argument");
+    if (R < 1 || k_in < 1 || k < 1) return fail(GR_EINVAL, "R, k_in, k must be >= 1");
+    if ((int64_t)R * k_in > 16384) return fail(GR_EINVAL, "R * k_in > 16384 not supported");
+    if (Q <= 0) return GR_OK;
+    GR_CUDA(cudaSetDevice(device));
+    const int sortcap = pow2ceil(R * k_in);
+    const int smem = sortcap * 12;
+    if (int rc = set_smem(merge_packed_kernel, smem)) return rc;
+    merge_packed_kernel<<<(unsigned)Q, GR_NT, smem, (cudaStream_t)stream>>>(in, R, Q, k_in, k, sortcap, out_ids,
+                                                                         out_scores, out_count);
     GR_CUDA(cudaGetLastError());
     return GR_OK;
 }

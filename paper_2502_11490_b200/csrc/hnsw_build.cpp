@@ -104,6 +104,24 @@ struct Builder {
         }
         return s;
     }
+    // the same sequential sums for up to 8 rows at once: independent dependency chains
+    // (each row's additions stay in order, so every result is bit-identical to dist2)
+    void dist2_x8(const int64_t *r, int n, const double *q, double *out) const {
+        const double *v[8];
+        for (int u = 0; u < 8; ++u) v[u] = row(r[u < n ? u : 0]);
+        double acc[8] = {0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0, 0.0};
+        for (int j = 0; j < dim; ++j) {
+            const double qj = q[j];
+#pragma GCC unroll 8
+            for (int u = 0; u < 8; ++u) {
+                const double t = v[u][j] - qj;
+                acc[u] += t * t;
+            }
+        }
+        for (int u = 0; u < n; ++u) out[u] = acc[u];
+    }
+    std::vector<int64_t> fresh;
+    std::vector<double> fresh_d;
 
     // numpy einsum('ij,ij->i') of one fp64 row d[0..K) with itself (oracle sqnorm_rows_f64)
     static double einsum_sq(const double *x, int K) {
@@ -127,6 +145,33 @@ struct Builder {
         const double *va = row(a), *vb = row(b);
         for (int j = 0; j < dim; ++j) diffs[j] = va[j] - vb[j];
         return einsum_sq(diffs.data(), dim);
+    }
+    // einsum_dist(a[u], b) for u < n <= 4, interleaved (each result identical to einsum_dist)
+    void einsum_dist_x4(const int64_t *a, int n, int64_t b, double *out) const {
+        const double *vb = row(b);
+        const double *va[4];
+        for (int u = 0; u < 4; ++u) va[u] = row(a[u < n ? u : 0]);
+        double l0[4] = {0.0, 0.0, 0.0, 0.0}, l1[4] = {0.0, 0.0, 0.0, 0.0};
+        const int nb = dim / 8;
+        for (int blk = 0; blk < nb; ++blk) {
+            const int p = 8 * blk;
+#pragma GCC unroll 4
+            for (int u = 0; u < 4; ++u) {
+                double x[8];
+                for (int t = 0; t < 8; ++t) x[t] = va[u][p + t] - vb[p + t];
+                double s0 = x[6] * x[6] + l0[u], s1 = x[7] * x[7] + l1[u];
+                s0 = x[4] * x[4] + s0; s1 = x[5] * x[5] + s1;
+                s0 = x[2] * x[2] + s0; s1 = x[3] * x[3] + s1;
+                l0[u] = x[0] * x[0] + s0; l1[u] = x[1] * x[1] + s1;
+            }
+        }
+        for (int p = 8 * nb; p < dim; p += 2)
+            for (int u = 0; u < 4; ++u) {
+                const double x0 = va[u][p] - vb[p], x1 = p + 1 < dim ? va[u][p + 1] - vb[p + 1] : 0.0;
+                l0[u] = x0 * x0 + l0[u];
+                l1[u] = x1 * x1 + l1[u];
+            }
+        for (int u = 0; u < n; ++u) out[u] = l0[u] + l1[u];
     }
 
     // kernels/_chot.pyx:116-179; returns (slots, dist2) ascending
@@ -154,11 +199,27 @@ struct Builder {
             if (res.n >= ef && before(res.d[0], res.i[0], d, node)) break;
             const int c = ct[node];
             const int32_t *r = nb + node * (int64_t)capl;
+            // stamp in row order and compute the distances of the unvisited neighbours first
+            // (pure), then run the reference's admission logic over them in the same order
+            fresh.clear();
             for (int j = 0; j < c; ++j) {
                 const int64_t v = r[j];
                 if (stamps[v] == stamp) continue;
                 stamps[v] = stamp;
-                const double dn = dist2(v, q);
+                fresh.push_back(v);
+            }
+            const int nf = (int)fresh.size();
+            fresh_d.resize(nf);
+            // rows are random accesses into a table far larger than the caches: start every
+            // line of every row now so the distance chains below stream from L1/L2
+            for (int j = 0; j < nf; ++j) {
+                const char *p = reinterpret_cast<const char *>(row(fresh[j]));
+                for (int b = 0; b < dim * 8; b += 64) __builtin_prefetch(p + b);
+            }
+            for (int j = 0; j < nf; j += 8) dist2_x8(fresh.data() + j, std::min(8, nf - j), q, fresh_d.data() + j);
+            for (int j = 0; j < nf; ++j) {
+                const int64_t v = fresh[j];
+                const double dn = fresh_d[j];
                 if (res.n >= ef && before(res.d[0], res.i[0], dn, v)) continue;
                 cand.push<false>(dn, v);
                 res.push<true>(dn, v);
@@ -222,7 +283,7 @@ struct Builder {
         cands.push_back(nw);
         const int nc = (int)cands.size();
         std::vector<double> d2(nc);
-        for (int j = 0; j < nc; ++j) d2[j] = einsum_dist(cands[j], nbr);
+        for (int j = 0; j < nc; j += 4) einsum_dist_x4(cands.data() + j, std::min(4, nc - j), nbr, d2.data() + j);
         std::vector<int> order(nc);
         for (int j = 0; j < nc; ++j) order[j] = j;
         std::stable_sort(order.begin(), order.end(), [&](int a, int b) {

@@ -51,12 +51,14 @@ struct SearchArgs {
     uint64_t *pool_key; // [slots][2][capP]
     int32_t *pool_slot; // [slots][2][capP]
     int32_t *pool_meta; // [slots][2][capP]: eval hop << 1 | exact (tensor-core mode)
-    unsigned long long *counters; // [0] exact re-scores, [1] tensor-core scores
+    unsigned long long *counters; // [0] exact re-scores, [1] tensor-core scores,
+                                  // [2] band violations, [3] max |approx - exact| / band (f32 bits)
     float band_rel, band_abs;     // refinement band: |s - T| <= band_rel*|T| + band_abs
     unsigned long long *phase_cycles; // nullable: per-phase SM cycles (instrumentation)
     int64_t capF, capS, capP;
     int *queue;
     int *nonfinite;
+    int *band_viol;  // violations since the last status read (tensor-core mode certificate)
     // shared-memory layout (byte offsets into dynamic smem)
     int off_w0, off_w[GR_MAX_MLP], off_b[GR_MAX_MLP], off_A, off_acc0, off_x0, off_h0, off_h1,
         off_score, off_hist, off_sortk, off_sortv, off_kp;
@@ -70,6 +72,28 @@ struct SearchArgs {
     int tma;
     CUtensorMap hl_map;
 };
+
+// Tensor-core mode certificate (run time).  The refinement argument (see below) needs
+// |approx - exact| < band/2 for every item.  Every exact re-score sees both values: it
+// records the largest ratio |approx - exact| / band(exact) and counts ratios above 1/2 in
+// the CTA's shared accumulators (bc[0] = count, bc[1] = max ratio as f32 bits); the host
+// re-runs the batch in exact mode when any violation was seen (gr_search).
+__device__ __forceinline__ void band_record(unsigned *bc, uint64_t approx_key, float exact,
+                                            float band_rel, float band_abs) {
+    const float ap = orderable_f32((uint32_t)(approx_key >> 32));
+    const float r = fabsf(ap - exact) / (band_rel * fabsf(exact) + band_abs);
+    if (!(r == r)) return;  // non-finite scores are reported by the nonfinite flag
+    if (r > 0.5f) atomicAdd(bc, 1u);
+    atomicMax(bc + 1, __float_as_uint(r));
+}
+__device__ __forceinline__ void band_flush(const unsigned *bc, unsigned long long *counters,
+                                           int *band_viol) {
+    if (bc[0]) {
+        atomicAdd(counters + 2, (unsigned long long)bc[0]);
+        atomicAdd(band_viol, (int)bc[0]);
+    }
+    if (bc[1]) atomicMax(counters + 3, (unsigned long long)bc[1]);
+}
 
 struct CtaState {
     int q;
@@ -127,11 +151,13 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ CtaState st;
     __shared__ unsigned long long ph_acc[8];
+    __shared__ unsigned bc[2];  // tensor-core band certificate (band_record)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const DevModel &M = a.M;
     // phase timing (thread 0, after the barrier that closes each phase)
     long long ph_t0 = 0;
     if (tid < 8) ph_acc[tid] = 0;
+    if (tid < 2) bc[tid] = 0u;
 #define GR_PH(i)                                                          \
     do {                                                                  \
         if (a.phase_cycles && tid == 0) {                                 \
@@ -429,6 +455,8 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
                     __syncthreads();
                     if (tid < nv) {
                         const int idx = rq[base + tid];
+                        band_record(bc, target == 0 ? pkey[pc][idx] : seg_key[idx], esc[tid],
+                                    a.band_rel, a.band_abs);
                         if (target == 0) {
                             pkey[pc][idx] = make_key(esc[tid], slot_rank(g, pslot[pc][idx]));
                             pmeta[pc][idx] |= 1;
@@ -753,6 +781,7 @@ __global__ void __launch_bounds__(GR_NT, MINB) hipanns_search_kernel(const Searc
     if constexpr (MODE == 1) {
         tc::fence_before();
         __syncthreads();
+        if (tid == 0) band_flush(bc, a.counters, a.band_viol);
         if (warp == 0)
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(128));
     }

@@ -384,9 +384,11 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
     unsigned char *const smem = PIPE ? smem_raw + ((1024u - (tc::smem_u32(smem_raw) & 1023u)) & 1023u) : smem_raw;
     __shared__ MqState<G> st;
     __shared__ unsigned long long ph_acc[16];
+    __shared__ unsigned bc[2];  // tensor-core band certificate (band_record)
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     long long ph_t0 = 0;
     if (tid < 16) ph_acc[tid] = 0;
+    if (tid < 2) bc[tid] = 0u;
 #define GR_PH(i)                                                          \
     do {                                                                  \
         if (a.phase_cycles && tid == 0) {                                 \
@@ -633,6 +635,8 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
                     if (tid < nv) {
                         const int e = rq[base + tid];
                         const int gq = e >> 24, idx = e & 0xFFFFFF;
+                        band_record(bc, pool ? pkey(gq, st.qs[gq].pool_cur)[idx] : seg_key[idx], sc[tid],
+                                    a.band_rel, a.band_abs);
                         if (pool) {
                             const int c = st.qs[gq].pool_cur;
                             pkey(gq, c)[idx] = make_key(sc[tid], slot_rank(g, pslot(gq, c)[idx]));
@@ -1060,6 +1064,7 @@ __global__ void __launch_bounds__(NT, (NT >= 512 ? 1 : 2)) hipanns_mq_kernel(con
     if constexpr (MODE == 1) {
         tc::fence_before();
         __syncthreads();
+        if (tid == 0) band_flush(bc, a.counters, a.band_viol);
         if (warp == 0)
             asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
     }

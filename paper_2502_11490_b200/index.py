@@ -202,7 +202,8 @@ class GraphIndex:
         k = self._n
         def grow(a, shape, dtype):
             new = np.zeros(shape, dtype=dtype)
-            new[:k] = a[:k]
+            c = min(k, len(a))  # loaded / wrapped indexes carry no stamps
+            new[:c] = a[:c]
             return new
         self._vectors = grow(self._vectors, (cap, self.dim), np.float64)
         self._ids = grow(self._ids, cap, np.int64)

@@ -38,6 +38,61 @@ class Workload:
     build_s: float
 
 
+def clustered_vectors(n: int, d: int, n_clusters: int, seed: int) -> np.ndarray:
+    """The reference's synthetic item features (nann/bench.py:24-28), same numpy stream."""
+    rng = np.random.default_rng(seed)
+    centers = rng.normal(scale=4.0, size=(n_clusters, d))
+    assign = rng.integers(0, n_clusters, size=n)
+    return centers[assign] + rng.normal(size=(n, d))
+
+
+def reference_inputs(name: str, n_queries: int | None = None):
+    """(model, item embeddings, user embeddings) of BASELINE config 1/2 exactly as the
+    reference recipe makes them: create_model(d, d, Z, (64, 64), seed=1),
+    items = item_embeddings(clustered_vectors(N, d, C, seed=0) as fp32), users =
+    user_embedding(default_rng(7).normal(size=(Q, d)) as fp32).  Bit-identical to the
+    reference's arrays (digests in tests/golden/cfg*_ref.npz)."""
+    N, d, m, C, Z, Q = CONFIGS[name]
+    model = create_model(d_x=d, d_h=d, z_dim=Z, hidden=(64, 64), seed=1)
+    emb = model.item_embeddings(clustered_vectors(N, d, C, seed=0).astype(np.float32))
+    users = model.user_embedding(
+        np.random.default_rng(7).normal(size=(n_queries or Q, d)).astype(np.float32))
+    return model, np.ascontiguousarray(emb), np.ascontiguousarray(users)
+
+
+def graph_digest(index: GraphIndex) -> str:
+    """sha256 over ids, levels, entry and every layer's rows in stored order (the same
+    digest tests/golden/make_cfg_golden.py records for the reference's build)."""
+    import hashlib
+
+    ids, levels, layers, entry = index.graph_view()
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(ids, dtype="<i8").tobytes())
+    h.update(np.ascontiguousarray(levels, dtype="<i4").tobytes())
+    h.update(np.int64(entry).tobytes())
+    n = len(ids)
+    for nb, ct in layers:
+        ct = np.asarray(ct[:n], dtype="<i4")
+        h.update(ct.tobytes())
+        mask = np.arange(nb.shape[1])[None, :] < ct[:, None]
+        h.update(np.asarray(nb[:n], dtype="<i4")[mask].tobytes())
+    return h.hexdigest()
+
+
+def make_reference(name: str, device: int = 0, n_queries: int | None = None) -> Workload:
+    """Config 1/2 on the reference's own inputs and graph: the index is the native exact
+    build (GraphIndex.build, identical to nann.GraphIndex.build(m=16, ef_construction=64,
+    seed=0)); items stay on the host too (CPU restatement / fixtures)."""
+    import torch
+
+    t0 = time.perf_counter()
+    N, d, m, C, Z, Q = CONFIGS[name]
+    model, emb, users = reference_inputs(name, n_queries)
+    index = GraphIndex.build(emb.astype(np.float64), m=m, ef_construction=64, seed=0)
+    items = torch.from_numpy(emb).to(torch.device("cuda", device))
+    return Workload(name, model, items, emb, users, index, time.perf_counter() - t0)
+
+
 def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
          n_queries: int | None = None, n_items: int | None = None) -> Workload:
     import torch
@@ -66,7 +121,7 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     users = (torch.randn(Q, d, generator=gu, device=dev) @ w_user).cpu().numpy()
     torch.backends.cuda.matmul.allow_tf32 = prev
     del centers, assign
-    index = GraphIndex.build(items, m=m, seed=0, device=dev)
+    index = GraphIndex.build(items, m=m, seed=0, device=dev, method="gpu")
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()  # hand the builder's cached blocks back before the search scratch
     items_host = items.cpu().numpy() if host_items else None
@@ -107,7 +162,7 @@ def make_shard(rank: int, world: int, shard_n: int = 12_500_000, d: int = 128, m
     del centers, assign
     lo = rank * shard_n
     index = GraphIndex.build(items, ids=np.arange(lo, lo + shard_n, dtype=np.int64), m=m,
-                             seed=rank, device=dev)
+                             seed=rank, device=dev, method="gpu")
     index.rows = np.arange(shard_n, dtype=np.int32)
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()

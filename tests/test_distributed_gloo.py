@@ -2,7 +2,8 @@
 
 Query partition: disjoint contiguous blocks covering the batch.  Catalog shards: each
 rank computes its shard's exact top-k (brute force over global ids, scored by the C
-oracle), the lists are all-gathered with the same `gather_lists` the NCCL path uses, and
+oracle), packed to the 8-byte wire format (fp32 score | u32 id, gr_pack_topk's layout) and
+all-gathered with the same single-collective `gather_packed` the NCCL path uses, and
 merging them with the reference pool semantics (CandidatePool) equals the global top-k.
 """
 
@@ -24,13 +25,32 @@ def _free_port():
     return p
 
 
+def _orderable(f32):
+    u = f32.view(np.uint32)
+    return np.where(u & 0x80000000, ~u, u | 0x80000000).astype(np.uint64)
+
+
+def pack_wire(ids, scores):
+    """Host statement of gr_pack_topk's format: orderable(fp32) << 32 | u32 id; 0 = empty."""
+    key = (_orderable(scores.astype(np.float32)) << np.uint64(32)) | ids.astype(np.uint64) & np.uint64(0xFFFFFFFF)
+    return np.where(ids < 0, np.uint64(0), key).view(np.int64)
+
+
+def unpack_wire(packed):
+    p = packed.view(np.uint64)
+    hi = (p >> np.uint64(32)).astype(np.uint32)
+    u = np.where(hi & 0x80000000, hi & 0x7FFFFFFF, ~hi).astype(np.uint32)
+    ids = np.where(p == 0, -1, (p & np.uint64(0xFFFFFFFF)).astype(np.int64))
+    return ids, u.view(np.float32).astype(np.float64)
+
+
 def _worker(rank, world, port, q):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from oracle import oracle_c
-        from paper_2502_11490_b200.distributed import block_range, gather_lists
+        from paper_2502_11490_b200.distributed import block_range, gather_packed
         from paper_2502_11490_b200 import CandidatePool, create_model
 
         rng = np.random.default_rng(0)
@@ -47,8 +67,9 @@ def _worker(rank, world, port, q):
             order = np.lexsort((np.arange(lo, hi), -s.astype(np.float64)))[:k]
             ids[qq, : len(order)] = torch.from_numpy(order + lo)
             sc[qq, : len(order)] = torch.from_numpy(s[order].astype(np.float64))
-        all_i, all_s = gather_lists(ids, sc)
-        assert tuple(all_i.shape) == (world, Q, k)
+        all_p = gather_packed(torch.from_numpy(pack_wire(ids.numpy(), sc.numpy())))
+        assert tuple(all_p.shape) == (world, Q, k)
+        all_i, all_s = unpack_wire(all_p.numpy())
         ok = True
         for qq in range(Q):
             pool = CandidatePool(k)
