@@ -87,8 +87,9 @@ def test_cfg1_brute_force_matches_reference(P):
     np.testing.assert_array_equal(scores, z["gt100_scores"])
 
 
-@pytest.mark.skipif(not os.path.exists(os.path.join(G.GOLDEN, "cfg2_ref.npz")),
-                    reason="cfg2 golden not generated")
+@pytest.mark.skipif(os.environ.get("GMPGR_CFG2_TESTS") != "1",
+                    reason="cfg2 (1M items) rebuilds the reference graph natively (minutes of host "
+                           "time): opt in with GMPGR_CFG2_TESTS=1")
 @pytest.mark.parametrize("mode", ["exact", "tc"])
 def test_cfg2_reference_inputs_match_reference(P, mode):
     check_against_golden(P, "cfg2", mode)
