@@ -79,17 +79,18 @@ def graph_digest(index: GraphIndex) -> str:
     return h.hexdigest()
 
 
-def make_reference(name: str, device: int = 0, n_queries: int | None = None) -> Workload:
+def make_reference(name: str, device: int | None = 0, n_queries: int | None = None) -> Workload:
     """Config 1/2 on the reference's own inputs and graph: the index is the native exact
     build (GraphIndex.build, identical to nann.GraphIndex.build(m=16, ef_construction=64,
-    seed=0)); items stay on the host too (CPU restatement / fixtures)."""
+    seed=0)); items stay on the host too (CPU restatement / fixtures); device=None keeps
+    everything on the host (the reference arm)."""
     import torch
 
     t0 = time.perf_counter()
     N, d, m, C, Z, Q = CONFIGS[name]
     model, emb, users = reference_inputs(name, n_queries)
     index = GraphIndex.build(emb.astype(np.float64), m=m, ef_construction=64, seed=0)
-    items = torch.from_numpy(emb).to(torch.device("cuda", device))
+    items = emb if device is None else torch.from_numpy(emb).to(torch.device("cuda", device))
     return Workload(name, model, items, emb, users, index, time.perf_counter() - t0)
 
 
