@@ -19,6 +19,7 @@
 #include "common.cuh"
 #include "search_kernel.cuh"
 #include "search_mq.cuh"
+#include "search_duo.cuh"
 #include "scores.cuh"
 
 namespace {
@@ -188,6 +189,24 @@ struct gr_searcher {
     unsigned long long *phase = nullptr; // [8] when GMPGR_PHASE_TIMING=1
     int *flags = nullptr; // [0] queue, [1] nonfinite, [2] bad index, [3] band violations
     int64_t launches = 0;
+    // duo-kernel scratch (search_duo.cuh): per unit lists, per query-slot bitsets/logs/pools
+    struct Duo {
+        int64_t units = 0, G = 0, capF = 0, capS = 0, capP = 0, hcap = 0, vwords = 0, logcap = 0;
+        int32_t *f_slot = nullptr, *f_srch = nullptr, *surv_v = nullptr, *surv_i = nullptr,
+                *cont_v = nullptr, *cont_i = nullptr, *fr_v = nullptr, *fr_i = nullptr,
+                *seg_v = nullptr, *pool_slot = nullptr, *pool_meta = nullptr, *vlog = nullptr;
+        uint64_t *fr_key = nullptr, *seg_key = nullptr, *pool_key = nullptr, *hash = nullptr;
+        uint32_t *vis = nullptr;
+        size_t bytes = 0;
+        void free_all() {
+            void *ps[] = {f_slot, f_srch, surv_v, surv_i, cont_v, cont_i, fr_v, fr_i, seg_v, pool_slot,
+                          pool_meta, vlog, fr_key, seg_key, pool_key, hash, vis};
+            for (void *p : ps)
+                if (p) cudaFree(p);
+            *this = Duo();
+        }
+    } duo;
+    int64_t duo_units_last = 0;  // resident units of the last duo launch (bench / tests)
     // staging for host-pointer calls
     DevBuf st_users, st_ids, st_scores, st_count, st_stats;
     size_t st_users_n = 0, st_out_n = 0, st_stats_n = 0;
@@ -977,6 +996,219 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     return GR_OK;
 }
 
+// ------------------------------------------------------------------ duo kernel
+// bytes of duo scratch per unit (lists x G queries, hash, per-query pools / bitsets / logs)
+size_t duo_unit_bytes(int64_t G, int64_t capF, int64_t capS, int64_t capP, int64_t hcap, int64_t vwords,
+                      int64_t logcap) {
+    const int64_t lF = capF * G, lS = capS * G;
+    return (size_t)(2 * 2 * lF * 4 + 7 * lS * 4 + 2 * lS * 8 + hcap * 8 + G * 2 * capP * 16 + G * vwords * 4 +
+                    G * logcap * 4);
+}
+
+int ensure_duo_scratch(gr_searcher *S, int64_t units, int64_t G, int64_t capF, int64_t capS, int64_t capP,
+                       int64_t hcap, int64_t vwords, int64_t logcap) {
+    gr_searcher::Duo &D = S->duo;
+    if (D.units >= units && D.G == G && D.capF >= capF && D.capS >= capS && D.capP >= capP && D.hcap >= hcap &&
+        D.vwords == vwords && D.logcap == logcap)
+        return GR_OK;
+    D.free_all();
+    const int64_t lF = capF * G, lS = capS * G, slots = units * G;
+    int rc = GR_OK;
+    if ((rc = dmalloc(&D.f_slot, (size_t)units * 2 * lF))) return rc;
+    if ((rc = dmalloc(&D.f_srch, (size_t)units * 2 * lF))) return rc;
+    int32_t **lists[] = {&D.surv_v, &D.surv_i, &D.cont_v, &D.cont_i, &D.fr_v, &D.fr_i, &D.seg_v};
+    for (int32_t **l : lists)
+        if ((rc = dmalloc(l, (size_t)units * lS))) return rc;
+    if ((rc = dmalloc(&D.fr_key, (size_t)units * lS))) return rc;
+    if ((rc = dmalloc(&D.seg_key, (size_t)units * lS))) return rc;
+    if ((rc = dmalloc(&D.hash, (size_t)units * hcap))) return rc;
+    if ((rc = dmalloc(&D.pool_key, (size_t)slots * 2 * capP))) return rc;
+    if ((rc = dmalloc(&D.pool_slot, (size_t)slots * 2 * capP))) return rc;
+    if ((rc = dmalloc(&D.pool_meta, (size_t)slots * 2 * capP))) return rc;
+    if ((rc = dmalloc(&D.vis, (size_t)slots * vwords))) return rc;
+    if ((rc = dmalloc(&D.vlog, (size_t)slots * logcap))) return rc;
+    GR_CUDA(cudaMemset(D.hash, 0xFF, (size_t)units * hcap * 8));
+    GR_CUDA(cudaMemset(D.vis, 0, (size_t)slots * vwords * 4));
+    D.units = units;
+    D.G = G;
+    D.capF = capF;
+    D.capS = capS;
+    D.capP = capP;
+    D.hcap = hcap;
+    D.vwords = vwords;
+    D.logcap = logcap;
+    D.bytes = duo_unit_bytes(G, capF, capS, capP, hcap, vwords, logcap) * units;
+    return GR_OK;
+}
+
+template <int DH, int ZZ, int MODE, int G>
+int plan_duo(int k, int kp, SearchArgs &a) {
+    using EX = ExactU<DH, ZZ>;
+    using TP = TcPipe2<DH, ZZ>;
+    a.sortcap = pow2ceil(std::max(k, kp));
+    const int hist_b = 8 * 256 * 4, sortk_b = G * a.sortcap * 8, sortv_b = G * a.sortcap * 4;
+    const int shared_b = MODE == 1 ? TP::B_BYTES : EX::W_END * 16;
+    auto up = [](int x, int al) { return (x + al - 1) / al * al; };
+    a.unit0 = up(shared_b, 1024);
+    SmemPlan U;  // unit-relative
+    int alias_end = 0;
+    if (MODE == 1) {
+        U.alloc(TP::UNIT_BYTES);  // A stages + barriers
+        alias_end = TP::A_REGION;
+    }
+    // exact buffers, histograms and pool sort live in the A stages when they fit (dead
+    // outside the scoring pipeline), else after them
+    int off = 0;
+    auto place = [&](int bytes) {
+        if (MODE == 1 && off + bytes <= alias_end) {
+            const int o = off;
+            off += (bytes + 15) & ~15;
+            return o;
+        }
+        return U.alloc(bytes);
+    };
+    a.off_x0 = place(EX::BUF_END * 16);
+    a.off_hist = place(hist_b);
+    a.off_sortk = place(sortk_b);
+    a.off_sortv = place(sortv_b);
+    a.off_misc = U.alloc((G * 64 + 64 + 64 * ZZ + 8) * 4);
+    a.off_acc0 = U.alloc(G * 64 * 16);
+    a.off_kp = U.alloc(3 * G * kp * 4);
+    a.unit_stride = up(U.bytes, 1024);
+    a.off_tmemp = a.unit0 + 2 * a.unit_stride;
+    return a.off_tmemp + 16 + 1024;  // + slack for the kernel's 1024-byte alignment of the carve
+}
+
+// Duo kernel for the fixed model shapes; returns -1 if not applicable
+int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I, const float *users,
+               int64_t Q, const gr_search_params *p, int64_t *ids, double *scores, int32_t *count,
+               int64_t *stats, cudaStream_t stream, int shape) {
+    SearchArgs a;
+    std::memset(&a, 0, sizeof(a));
+    const int mode = p->mode;
+    if (mode == GR_MODE_TC && I->di.hl == nullptr) return -1;
+    constexpr int GQ = 8;
+    int smem = 0;
+    void (*kern)(const SearchArgs) = nullptr;
+#define GR_DUO_CASE(CODE, DH, ZZ)                                            \
+    case CODE:                                                               \
+        if (mode == GR_MODE_TC) {                                            \
+            smem = plan_duo<DH, ZZ, 1, GQ>(p->k, p->k_parallel, a);          \
+            kern = hipanns_duo_kernel<DH, ZZ, 1, GQ>;                        \
+        } else {                                                             \
+            smem = plan_duo<DH, ZZ, 0, GQ>(p->k, p->k_parallel, a);          \
+            kern = hipanns_duo_kernel<DH, ZZ, 0, GQ>;                        \
+        }                                                                    \
+        break;
+    switch (shape) {
+        GR_DUO_CASE(1283, 128, 3)
+        GR_DUO_CASE(1282, 128, 2)
+        GR_DUO_CASE(643, 64, 3)
+        GR_DUO_CASE(642, 64, 2)
+    default: return -1;
+    }
+#undef GR_DUO_CASE
+    if (smem > kMaxSmem) return -1;
+    // lists: re-score requests pack (query << 24 | index) with index < capS * G or < capP
+    const int64_t capF = (int64_t)p->k_parallel * p->ef;
+    const int64_t capS = std::max<int64_t>(std::min<int64_t>(capF * G->max_deg, (int64_t)p->k_parallel * G->dg.n),
+                                           G->max_deg + 1) + 64;
+    const int64_t capP = p->k + capS;
+    if (capS * GQ >= (1 << 24) || capP >= (1 << 24)) return -1;
+    int64_t hcap = 64;
+    while (hcap < 2 * capS * GQ) hcap <<= 1;
+    const int64_t vwords = (G->dg.n + 15) / 16;
+    const int64_t logcap = std::min<int64_t>(G->dg.n + 1, 1 << 16);
+    if (int rc = set_smem(kern, smem)) return rc;
+    int per_sm = 0;
+    GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 512, smem));
+    if (per_sm < 1) return -1;
+    // resident units: enough for the batch, at most one CTA per SM, and within the scratch
+    // memory budget (free device memory + what this searcher already holds, times
+    // GMPGR_SCRATCH_FRAC (default 0.8), or GMPGR_SCRATCH_GB)
+    int64_t units = std::min<int64_t>((Q + GQ - 1) / GQ, 2LL * per_sm * num_sms(G->device));
+    units = (units + 1) & ~1LL;
+    const size_t per_unit = duo_unit_bytes(GQ, capF, capS, capP, hcap, vwords, logcap);
+    size_t budget = 0;
+    if (const char *gb = getenv("GMPGR_SCRATCH_GB")) {
+        budget = (size_t)(atof(gb) * 1e9);
+    } else {
+        size_t fr = 0, tot = 0;
+        GR_CUDA(cudaMemGetInfo(&fr, &tot));
+        double frac = 0.8;
+        if (const char *f = getenv("GMPGR_SCRATCH_FRAC")) frac = atof(f);
+        budget = (size_t)((double)(fr + S->duo.bytes) * frac);
+    }
+    units = std::min<int64_t>(units, (int64_t)(budget / per_unit) & ~1LL);
+    if (units < 2)
+        return fail(GR_ENOMEM, "search scratch for one CTA (" + std::to_string(2 * per_unit) +
+                                   " bytes) exceeds the device memory budget");
+    if (int rc = ensure_duo_scratch(S, units, GQ, capF, capS, capP, hcap, vwords, logcap)) return rc;
+    S->duo_units_last = units;
+    const gr_searcher::Duo &D = S->duo;
+    a.g = G->dg;
+    a.M = M->dm;
+    a.it = I->di;
+    std::unique_lock<std::mutex> hl_lock;
+    if (mode == GR_MODE_TC) {
+        int64_t rows = I->di.n;
+        if (G->dg.rows) {  // slot-ordered copy (the graph's BFS order) when slots != rows
+            hl_lock = std::unique_lock<std::mutex>(const_cast<gr_graph *>(G)->hl_mu);
+            if (int rc = ensure_slot_hl(const_cast<gr_graph *>(G), I, stream)) return rc;
+            a.it.hl = G->hl_slot;
+            a.it.hl_by_slot = 1;
+            rows = G->dg.n;
+        }
+        if (int rc = make_hl_map(&a.hl_map, a.it.hl, rows, I->di.d)) return rc;
+        a.tma = 1;
+    }
+    a.users = users;
+    a.Q = Q;
+    a.k = p->k;
+    a.kp = p->k_parallel;
+    a.hops = p->hops;
+    a.ef = p->ef;
+    a.out_ids = ids;
+    a.out_scores = scores;
+    a.out_count = count;
+    a.out_stats = stats;
+    a.f_slot = D.f_slot;
+    a.f_srch = D.f_srch;
+    a.surv_v = D.surv_v;
+    a.surv_i = D.surv_i;
+    a.cont_v = D.cont_v;
+    a.cont_i = D.cont_i;
+    a.fr_v = D.fr_v;
+    a.fr_i = D.fr_i;
+    a.fr_key = D.fr_key;
+    a.seg_v = D.seg_v;
+    a.seg_key = D.seg_key;
+    a.pool_key = D.pool_key;
+    a.pool_slot = D.pool_slot;
+    a.pool_meta = D.pool_meta;
+    a.hash = D.hash;
+    a.hash_cap = D.hcap;
+    a.vis = D.vis;
+    a.vis_words = D.vwords;
+    a.vlog = D.vlog;
+    a.log_cap = (int)D.logcap;
+    a.counters = S->counters;
+    a.phase_cycles = S->phase;
+    a.band_rel = p->band_rel > 0.f ? p->band_rel : 1e-3f;
+    a.band_abs = p->band_abs > 0.f ? p->band_abs : 1e-3f;
+    a.capF = D.capF * GQ;  // unit-level flattened lists
+    a.capS = D.capS * GQ;
+    a.capP = D.capP;       // per-query pools
+    a.queue = S->flags;
+    a.nonfinite = S->flags + 1;
+    a.band_viol = S->flags + 3;
+    GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
+    kern<<<(int)(units / 2), 512, smem, stream>>>(a);
+    GR_CUDA(cudaGetLastError());
+    S->launches += 1;
+    return GR_OK;
+}
+
 // approximate (first-pass) tensor-core scores of one user against item rows: error studies
 template <int DH, int ZZ>
 __global__ void __launch_bounds__(GR_NT, 1) tc_pairs_kernel(DevModel M, DevItems it, const float *user,
@@ -1042,9 +1274,16 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     const int mode = p->mode;
     if (mode == GR_MODE_TC && (!shape || !M->dm.tc_ok))
         return fail(GR_EINVAL, "tensor-core mode needs the (d_h in {64,128}, hidden (64,64), Z in {2,3}) model shape");
-    // fixed shapes run the multi-query kernel unless GMPGR_KERNEL=cta selects the per-query one
+    // fixed shapes run the duo kernel (two 256-thread units per CTA, bitset visited state);
+    // GMPGR_KERNEL=mq selects the round-1 lock-step multi-query kernel (per-slot N-wide claim
+    // tags), GMPGR_KERNEL=cta the per-query kernel
     const char *kenv = getenv("GMPGR_KERNEL");
-    if (shape && !(kenv && std::strcmp(kenv, "cta") == 0)) {
+    const bool k_cta = kenv && std::strcmp(kenv, "cta") == 0, k_mq = kenv && std::strcmp(kenv, "mq") == 0;
+    if (shape && !k_cta && !k_mq) {
+        const int rc = launch_duo(S, G, M, I, users, Q, p, ids, scores, count, stats, stream, shape);
+        if (rc != -1) return rc;
+    }
+    if (shape && !k_cta) {
         const int rc = launch_mq(S, G, M, I, users, Q, p, ids, scores, count, stats, stream, shape);
         if (rc != -1) return rc;
     }
@@ -1225,6 +1464,7 @@ int gr_searcher_destroy(gr_searcher *s) {
         cudaDeviceSynchronize();
     }
     s->free_scratch();
+    s->duo.free_all();
     cudaFree(s->flags);
     cudaFree(s->counters);
     if (s->done) cudaEventDestroy(s->done);

@@ -71,6 +71,15 @@ struct SearchArgs {
     // (GMPGR_TMA), else per-thread cp.async
     int tma;
     CUtensorMap hl_map;
+    // duo kernel (search_duo.cuh): two units per CTA, bitset visited state
+    int unit0, unit_stride, off_misc, off_tmemp;  // shared-memory plan (bytes)
+    int32_t *cont_v, *cont_i;  // [units][capS] contested touches
+    uint64_t *hash;            // [units][hash_cap] (query, node) -> survivor index
+    int64_t hash_cap;
+    uint32_t *vis;             // [units * G][vis_words]: 2 bits per node (D, T)
+    int64_t vis_words;
+    int32_t *vlog;             // [units * G][log_cap]: claimed nodes of the running query
+    int log_cap;
 };
 
 // Tensor-core mode certificate (run time).  The refinement argument (see below) needs

@@ -1,0 +1,255 @@
+// Warp-specialised tcgen05 scoring pipeline for ONE 256-thread unit of the duo kernel
+// (search_duo.cuh: a 512-thread CTA runs two independent units, each with its own queries,
+// barriers and pipeline, sharing the weight operands in shared memory and one TMEM
+// allocation).  Same arithmetic as tc_pipe.cuh (split-bf16 "bf16x3": hi.[W_hi; W_lo] as one
+// N=128 MMA + lo.W_hi per k-step, layer-1 A operand in TMEM via the ".ts" form), with the
+// roles of a unit:
+//   warps 0-3  epilogue (one group; warp w reads TMEM lanes 32*(w&3)..: one pair row per thread)
+//   warp 4     tcgen05.mma issuer (converged warp, elect.sync issues)
+//   warps 5-7  TMA loaders: per 64-wide K chunk of a 128-pair tile, 64 tile::gather4 ops
+//              (32 four-row groups x hi/lo halves, 128-byte swizzled rows) over 96 lanes
+// Buffers per unit: S = 2 stages of one K chunk of the A operand (hi + lo, 32 KB each) in
+// shared memory; TMEM window of 256 columns: D0 [0,128) (layer 0: [0,64) = hi.W_hi + lo.W_hi,
+// [64,128) = hi.W_lo), D1 [128,192) (layer 1), A1 [192,256) (relu(layer 0) as bf16 hi|lo pairs).
+// Hand-offs (mbarriers): full[s] (TMA tx) -> issuer, empty[s] commit -> loaders,
+// d0full commit -> E, d0empty E -> issuer, a1full E -> issuer, d1full commit -> E.
+// The single epilogue group serialises D0 / A1 / D1 reuse by program order.
+#pragma once
+#include <cuda_bf16.h>
+
+#include "common.cuh"
+#include "tc_scorer.cuh"
+
+template <int D_H, int Z>
+struct TcPipe2 {
+    static constexpr int H = 64, TM = 128, KC = 64, NC = D_H / KC, S = 2;
+    static constexpr int NT = 256, NE = 128, ISSUER_WARP = 4, L_WARP0 = 5, NLW = 3;
+    static constexpr int NOPS = 2 * TM / 4;  // TMA gather4 ops per K chunk (hi + lo)
+    // shared (both units) weight operands, at the CTA carve base
+    static constexpr int OFF_B0H = 0;
+    static constexpr int OFF_B0L = OFF_B0H + H * D_H * 2;
+    static constexpr int OFF_B1H = OFF_B0L + H * D_H * 2;
+    static constexpr int OFF_B1L = OFF_B1H + H * H * 2;
+    static constexpr int B_BYTES = OFF_B1L + H * H * 2;
+    // per-unit block (1024-aligned: SWIZZLE_128B stages)
+    static constexpr int CH_BYTES = TM * KC * 2;                // one hi or lo chunk: 16 KB
+    static constexpr int OFF_A = 0;                             // S chunk stages (hi, lo)
+    static constexpr int A_REGION = S * 2 * CH_BYTES;           // 64 KB, aliased outside run()
+    static constexpr int OFF_BAR = OFF_A + A_REGION;
+    enum { FULL0 = 0, EMPTY0 = S, D0FULL = 2 * S, D0EMPTY, A1FULL, D1FULL, NBAR };
+    static constexpr int UNIT_BYTES = ((OFF_BAR + NBAR * 8 + 1023) / 1024) * 1024;
+    static constexpr uint32_t IDESC = tc::idesc(TM, H);
+    static constexpr uint32_t IDESC_N128 = tc::idesc(TM, 2 * H);
+    static constexpr uint32_t C_D0 = 0, C_D1 = 128, C_A1 = 192, COLS = 256;
+
+    static __device__ __forceinline__ uint64_t *bar(unsigned char *u, int i) {
+        return reinterpret_cast<uint64_t *>(u + OFF_BAR) + i;
+    }
+
+    // lt: thread index inside the unit
+    static __device__ void init_barriers(unsigned char *u, int lt) {
+        if (lt == 0) {
+            for (int s = 0; s < S; ++s) {
+                tc::mbar_init(bar(u, FULL0 + s), NOPS);
+                tc::mbar_init(bar(u, EMPTY0 + s), 1);
+            }
+            tc::mbar_init(bar(u, D0FULL), 1);
+            tc::mbar_init(bar(u, D0EMPTY), NE);
+            tc::mbar_init(bar(u, A1FULL), NE);
+            tc::mbar_init(bar(u, D1FULL), 1);
+        }
+    }
+
+    // Score pairs [0, n) of this unit: item slot slots[i], pair tag gis[i] (query << 16 |
+    // searcher).  Every epilogue thread calls on_score(i, valid, score, gi, slot) per row
+    // (all 32 lanes of its warp together).  sm: CTA carve base (weights); u: this unit's
+    // block; misc: U [G][64] (user half + b0), b1[64], W2[Z][64], b2[4], att[4] (shared
+    // memory); tmem: this unit's TMEM window; chunk_ctr / tile_ctr: unit-lifetime counters;
+    // sync(): the unit's barrier.
+    template <class OnScore, class Sync>
+    static __device__ __forceinline__ void run(unsigned char *sm, unsigned char *u, const float *U,
+                                               const float *b1, const float *W2, const float *b2,
+                                               const float *att, uint32_t tmem, const DevItems &it,
+                                               const DevGraph &g, const int32_t *slots, const int32_t *gis,
+                                               int n, uint32_t &chunk_ctr, uint32_t &tile_ctr, int lt,
+                                               OnScore on_score, Sync sync, const void *tmap) {
+        const int warp = lt >> 5, lane = lt & 31;
+        const int T = (n + TM - 1) / TM;
+        if (T == 0) return;
+        // the A stages alias generic-proxy buffers outside run(): order those accesses before
+        // the TMA (async-proxy) writes into them
+        tc::fence_async_smem();
+        sync();
+        if (warp >= L_WARP0) {
+            const int lw = warp - L_WARP0, o = lane * NLW + lw;
+            if (o < NOPS) {
+                const int grp = o >> 1, half = o & 1;
+                auto rows_of = [&](int t, int (&dst)[4]) {
+                    const int base = t * TM, nv = t < T ? min(TM, n - base) : 0;
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int r = 4 * grp + j;
+                        const int32_t sl = r < nv ? slots[base + r] : -1;
+                        dst[j] = sl < 0 ? 0 : (it.hl_by_slot ? (int)sl : (int)slot_row(g, sl));
+                    }
+                };
+                int nx[4];
+                rows_of(0, nx);
+                for (int t = 0; t < T; ++t) {
+                    int cur[4];
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) cur[j] = nx[j];
+                    if (t + 1 < T) rows_of(t + 1, nx);
+#pragma unroll
+                    for (int kc = 0; kc < NC; ++kc) {
+                        const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, r = qg / S;
+                        if (r >= 1) tc::mbar_wait(bar(u, EMPTY0 + s), (r - 1) & 1u);
+                        tc::mbar_arrive_expect_tx(bar(u, FULL0 + s), 512);
+                        tc::tma_gather4(tc::smem_u32(u + OFF_A + s * 2 * CH_BYTES) + half * CH_BYTES + grp * 512,
+                                        tmap, half * D_H + kc * KC, cur[0], cur[1], cur[2], cur[3],
+                                        bar(u, FULL0 + s));
+                    }
+                }
+            }
+        } else if (warp == ISSUER_WARP) {
+            constexpr unsigned FULLM = 0xffffffffu;
+            const uint32_t bH0 = tc::smem_u32(sm + OFF_B0H);
+            const uint32_t bH1 = tc::smem_u32(sm + OFF_B1H), bL1 = tc::smem_u32(sm + OFF_B1L);
+            auto ready = [&](int b, uint32_t par) {
+                return __shfl_sync(FULLM, lane == 0 ? (int)tc::mbar_test(bar(u, b), par) : 0, 0) != 0;
+            };
+            int l0t = 0, l0k = 0, l1t = 0;
+            while (l1t < T) {
+                if (l1t < l0t) {  // layer 1 of an earlier tile as soon as its A1 is in TMEM
+                    const uint32_t tg = tile_ctr + l1t;
+                    if (ready(A1FULL, tg & 1u)) {
+                        tc::fence_after();
+                        const uint32_t a1 = tmem + C_A1, d1 = tmem + C_D1;
+#pragma unroll
+                        for (int k = 0; k < H / 16; ++k) {
+                            const uint64_t bh = tc::desc(bH1 + k * 256, H), bl = tc::desc(bL1 + k * 256, H);
+                            tc::mma_ts_w(d1, a1 + k * 8, bh, IDESC, k ? 1u : 0u);       // hi . hi
+                            tc::mma_ts_w(d1, a1 + k * 8, bl, IDESC, 1u);                // hi . lo
+                            tc::mma_ts_w(d1, a1 + 32 + k * 8, bh, IDESC, 1u);           // lo . hi
+                        }
+                        tc::commit_w(bar(u, D1FULL));
+                        ++l1t;
+                        continue;
+                    }
+                }
+                if (l0t < T) {
+                    const uint32_t tg = tile_ctr + l0t;
+                    const uint32_t qg = chunk_ctr + l0t * NC + l0k, s = qg % S, r = qg / S;
+                    // D0 of the previous tile must have been read by the epilogue
+                    if ((l0k != 0 || tg == 0 || ready(D0EMPTY, (tg - 1) & 1u)) && ready(FULL0 + s, r & 1u)) {
+                        tc::fence_async_smem();
+                        tc::fence_after();
+                        const uint32_t d0 = tmem + C_D0;
+                        const uint32_t aH = tc::smem_u32(u + OFF_A + s * 2 * CH_BYTES), aL = aH + CH_BYTES;
+#pragma unroll
+                        for (int k = 0; k < KC / 16; ++k) {
+                            const uint64_t ah = tc::desc_sw128(aH + k * 32), al = tc::desc_sw128(aL + k * 32);
+                            const uint32_t kb = (l0k * (KC / 16) + k) * 256;
+                            const uint64_t bh = tc::desc(bH0 + kb, D_H);
+                            tc::mma_w(d0, ah, bh, IDESC_N128, (l0k | k) ? 1u : 0u);  // hi . [W_hi; W_lo]
+                            tc::mma_w(d0, al, bh, IDESC, 1u);                          // lo . W_hi
+                        }
+                        tc::commit_w(bar(u, EMPTY0 + s));
+                        if (++l0k == NC) {
+                            tc::commit_w(bar(u, D0FULL));
+                            l0k = 0;
+                            ++l0t;
+                        }
+                    }
+                }
+            }
+            __syncwarp();
+        } else {
+            // ================= epilogue: row = TMEM lane
+            const int q4 = warp & 3, row = q4 * 32 + lane;
+            const uint32_t lanebase = (uint32_t)(q4 * 32) << 16;
+            for (int t = 0; t < T; ++t) {
+                const uint32_t tg = tile_ctr + t;
+                const int base = t * TM, nv = min(TM, n - base);
+                const int gi = row < nv ? gis[base + row] : 0, gq = gi >> 16;
+                const int32_t my_s = row < nv ? slots[base + row] : 0;
+                const float *uq = U + gq * H;
+                tc::mbar_wait(bar(u, D0FULL), tg & 1u);
+                tc::fence_after();
+                float h[64];
+                {
+                    const uint32_t d0 = tmem + lanebase + C_D0;
+#pragma unroll
+                    for (int half = 0; half < 2; ++half) {
+                        float va[32], vb[32];
+                        tc::tmem_ld32(d0 + 32 * half, va);
+                        tc::tmem_ld32(d0 + 64 + 32 * half, vb);
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) h[32 * half + j] = va[j] + vb[j];
+                    }
+                }
+                tc::fence_before();
+                tc::mbar_arrive(bar(u, D0EMPTY));
+                const uint32_t a1 = tmem + lanebase + C_A1;
+#pragma unroll
+                for (int o = 0; o < 64; o += 16) {
+                    uint32_t hi[8], lo[8];
+#pragma unroll
+                    for (int j = 0; j < 16; j += 4) {
+                        const float4 uo = *reinterpret_cast<const float4 *>(uq + o + j);
+                        const float y0 = fmaxf(h[o + j] + uo.x, 0.f), y1 = fmaxf(h[o + j + 1] + uo.y, 0.f);
+                        const float y2 = fmaxf(h[o + j + 2] + uo.z, 0.f), y3 = fmaxf(h[o + j + 3] + uo.w, 0.f);
+                        uint2 hh, ll;
+                        tc::split4(make_float4(y0, y1, y2, y3), hh, ll);
+                        hi[j / 2] = hh.x; hi[j / 2 + 1] = hh.y;
+                        lo[j / 2] = ll.x; lo[j / 2 + 1] = ll.y;
+                    }
+                    tc::tmem_st8(a1 + o / 2, hi);
+                    tc::tmem_st8(a1 + 32 + o / 2, lo);
+                }
+                tc::tmem_wait_st();
+                tc::fence_before();
+                tc::mbar_arrive(bar(u, A1FULL));
+                tc::mbar_wait(bar(u, D1FULL), tg & 1u);
+                tc::fence_after();
+                {
+                    float va[32], vb[32];
+                    tc::tmem_ld32(tmem + lanebase + C_D1, va);
+                    tc::tmem_ld32(tmem + lanebase + C_D1 + 32, vb);
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) { h[j] = fmaxf(va[j] + b1[j], 0.f); h[32 + j] = fmaxf(vb[j] + b1[32 + j], 0.f); }
+                }
+                tc::fence_before();
+                // approximate path (reassociated): the exact refinement re-scores every item
+                // near a threshold, and the band certificate checks the error at run time
+                float s = 0.f;
+                bool bad = false;
+                const float4 *W2v = reinterpret_cast<const float4 *>(W2);
+                float zp[Z][4];
+#pragma unroll
+                for (int o = 0; o < Z; ++o) zp[o][0] = zp[o][1] = zp[o][2] = zp[o][3] = 0.f;
+#pragma unroll
+                for (int j = 0; j < 64; j += 4) {
+#pragma unroll
+                    for (int o = 0; o < Z; ++o) {
+                        const float4 w = W2v[o * (H / 4) + j / 4];
+                        zp[o][0] = fmaf(h[j], w.x, zp[o][0]);
+                        zp[o][1] = fmaf(h[j + 1], w.y, zp[o][1]);
+                        zp[o][2] = fmaf(h[j + 2], w.z, zp[o][2]);
+                        zp[o][3] = fmaf(h[j + 3], w.w, zp[o][3]);
+                    }
+                }
+#pragma unroll
+                for (int o = 0; o < Z; ++o) {
+                    const float z = b2[o] + ((zp[o][0] + zp[o][1]) + (zp[o][2] + zp[o][3]));
+                    bad |= !isfinite(z);
+                    s = fmaf(z, att[o], s);
+                }
+                on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s, gi, my_s);
+            }
+        }
+        chunk_ctr += T * NC;
+        tile_ctr += T;
+        sync();
+    }
+};
