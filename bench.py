@@ -292,7 +292,7 @@ def run_gmpgr(args):
     model, index = wl.model, wl.index
     metric = model.metric
     dm = metric.device_model(dev)
-    g = index.device_graph(dev)
+    g = index.device_graph(dev, items=wl.items)
     it = _lib.DeviceItems(wl.items, dev)
     searcher = _lib.DeviceSearcher(dev)
     Q, k, L, d_h = len(wl.users), PARAMS["k"], g.n_layers, model.d_h

@@ -96,6 +96,15 @@ int gr_model_destroy(gr_model *m);
 int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *nbrs,
                     const int64_t *row_stride, const int32_t *const *cnts, const int32_t *levels,
                     int32_t entry_slot, const int64_t *ids, const int32_t *rows, gr_graph **out);
+/* Same, with the device slot order chosen by the caller: order int64 [n] lists the caller
+ * slots in device-slot order (a permutation; NULL = the default breadth-first order from the
+ * entry).  Device slot order is invisible to results (ids and the id-rank tie-break are
+ * carried per slot); it sets the memory locality of the per-query visited state, the
+ * adjacency rows and the slot-ordered embedding copy (e.g. cluster-contiguous orders). */
+int gr_graph_create_ordered(int device, int n_layers, int64_t n, const int32_t *const *nbrs,
+                            const int64_t *row_stride, const int32_t *const *cnts,
+                            const int32_t *levels, int32_t entry_slot, const int64_t *ids,
+                            const int32_t *rows, const int64_t *order, gr_graph **out);
 int gr_graph_destroy(gr_graph *g);
 
 /* Item embeddings fp32 [n, d] row-major (host or device pointer per emb_on_device). */

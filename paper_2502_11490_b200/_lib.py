@@ -23,7 +23,7 @@ GR_OK, GR_EINVAL, GR_ENUMERIC, GR_ECUDA, GR_ENOMEM, GR_EBAND = 0, 1, 2, 3, 4, 5
 EXPORTS = (
     "gr_last_error", "gr_abi_version", "gr_device_count",
     "gr_model_create", "gr_model_destroy",
-    "gr_graph_create", "gr_graph_destroy",
+    "gr_graph_create", "gr_graph_create_ordered", "gr_graph_destroy",
     "gr_items_create", "gr_items_destroy",
     "gr_score_pairs", "gr_score_items_approx",
     "gr_searcher_create", "gr_searcher_destroy",
@@ -59,6 +59,7 @@ def _declare(lib):
         "gr_model_create": (C.c_int, [C.c_int, C.c_int, vp, vp, vp, vp, C.c_int, vp]),
         "gr_model_destroy": (C.c_int, [vp]),
         "gr_graph_create": (C.c_int, [C.c_int, C.c_int, i64, vp, vp, vp, vp, i32, vp, vp, vp]),
+        "gr_graph_create_ordered": (C.c_int, [C.c_int, C.c_int, i64, vp, vp, vp, vp, i32, vp, vp, vp, vp]),
         "gr_graph_destroy": (C.c_int, [vp]),
         "gr_items_create": (C.c_int, [C.c_int, vp, i64, i32, C.c_int, vp]),
         "gr_items_destroy": (C.c_int, [vp]),
@@ -192,7 +193,8 @@ class DeviceGraph(_Handle):
     """gr_graph: device layout of GraphIndex.graph_view() (index.py:384-391)."""
     _destroy = "gr_graph_destroy"
 
-    def __init__(self, layers, levels, entry_slot, ids, rows=None, device: int | None = None):
+    def __init__(self, layers, levels, entry_slot, ids, rows=None, device: int | None = None,
+                 order=None):
         require_device()
         device = current_device() if device is None else device
         n = len(ids)
@@ -204,10 +206,13 @@ class DeviceGraph(_Handle):
         rows = None if rows is None else np.ascontiguousarray(rows, dtype=np.int32)
         self.n = n
         self.n_layers = len(layers)
+        order = None if order is None else np.ascontiguousarray(order, dtype=np.int64)
+        if order is not None and order.shape != (n,):
+            raise InvalidArgumentError("order must list every slot once")
         h = C.c_void_p()
-        check(lib().gr_graph_create(device, len(layers), n, ptr_array(nbrs), ptr(stride),
-                                    ptr_array(cnts), ptr(levels), int(entry_slot), ptr(ids),
-                                    ptr(rows), C.byref(h)))
+        check(lib().gr_graph_create_ordered(device, len(layers), n, ptr_array(nbrs), ptr(stride),
+                                            ptr_array(cnts), ptr(levels), int(entry_slot), ptr(ids),
+                                            ptr(rows), ptr(order), C.byref(h)))
         super().__init__(h, device)
 
 

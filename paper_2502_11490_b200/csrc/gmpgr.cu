@@ -358,6 +358,14 @@ int gr_model_destroy(gr_model *m) {
 int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *nbrs,
                     const int64_t *row_stride, const int32_t *const *cnts, const int32_t *levels,
                     int32_t entry_slot, const int64_t *ids, const int32_t *rows, gr_graph **out) {
+    return gr_graph_create_ordered(device, n_layers, n, nbrs, row_stride, cnts, levels, entry_slot, ids, rows,
+                                   nullptr, out);
+}
+
+int gr_graph_create_ordered(int device, int n_layers, int64_t n, const int32_t *const *nbrs,
+                            const int64_t *row_stride, const int32_t *const *cnts, const int32_t *levels,
+                            int32_t entry_slot, const int64_t *ids, const int32_t *rows, const int64_t *order,
+                            gr_graph **out) {
     if (!out || !nbrs || !row_stride || !cnts || !ids) return fail(GR_EINVAL, "null argument");
     if (n < 1) return fail(GR_EINVAL, "index is empty");
     if (n > 0x7ffffff0LL) return fail(GR_EINVAL, "more than 2^31 slots");
@@ -385,7 +393,15 @@ int gr_graph_create(int device, int n_layers, int64_t n, const int32_t *const *n
     // reported by id and every tie-break uses the id rank, never the slot.
     std::vector<int64_t> perm;  // device slot -> caller slot (empty = identity)
     std::vector<int32_t> inv;   // caller slot -> device slot
-    {
+    if (order) {  // caller-provided locality order (a permutation of the slots)
+        perm.assign(order, order + n);
+        inv.assign(n, -1);
+        for (int64_t s = 0; s < n; ++s) {
+            const int64_t o = perm[s];
+            if (o < 0 || o >= n || inv[o] >= 0) return cleanup(fail(GR_EINVAL, "order is not a permutation of the slots"));
+            inv[o] = (int32_t)s;
+        }
+    } else {
         const char *renv = getenv("GMPGR_REORDER");
         if (!(renv && std::strcmp(renv, "0") == 0) && n > 1) {
             perm.reserve(n);

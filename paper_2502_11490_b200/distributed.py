@@ -109,7 +109,7 @@ class ShardedSearcher:
         self.metric = getattr(model, "metric", model)
         self.device = _lib.current_device() if device is None else device
         self.dm = self.metric.device_model(self.device)
-        self.graph = shard_index.device_graph(self.device)
+        self.graph = shard_index.device_graph(self.device, items=shard_items)
         self.items = device_items(shard_items, self.device)
         self.searcher = _lib.DeviceSearcher(self.device)
         self.group = group

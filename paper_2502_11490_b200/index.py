@@ -23,6 +23,7 @@ from .errors import FileFormatError, InvalidArgumentError
 INDEX_MAGIC = b"NANN-IDX"
 INDEX_VERSION = 1
 _HEAD_FMT = "<IIIIdBqQIIq"  # version, L, m, efc, p, heuristic, seed, ordinal, n, dim, entry
+LOCALITY_MIN = 1 << 16  # slots below this: breadth-first device order (fits caches anyway)
 
 
 class GraphIndex:
@@ -378,14 +379,28 @@ class GraphIndex:
         return idx
 
     # ---------------------------------------------------------------- device
-    def device_graph(self, device: int | None = None) -> _lib.DeviceGraph:
-        """Cached gr_graph upload of graph_view() (invalidated by no mutation: read side only)."""
+    def device_graph(self, device: int | None = None, items=None) -> _lib.DeviceGraph:
+        """Cached gr_graph upload of graph_view() (invalidated by no mutation: read side only).
+
+        With the item embeddings at hand (the search entry points pass them) and at least
+        LOCALITY_MIN slots, device slots are grouped by embedding cluster (locality.py);
+        otherwise breadth-first from the entry.  GMPGR_ORDER=bfs forces the latter."""
+        import os
+
         device = _lib.current_device() if device is None else device
         h = self._dev.get(device)
         if h is None:
             if self._n == 0:
                 raise InvalidArgumentError("index is empty")
             ids, levels, layers, entry = self.graph_view()
-            h = _lib.DeviceGraph(layers, levels, entry, ids, rows=self.rows, device=device)
+            order = None
+            if (items is not None and self._n >= LOCALITY_MIN
+                    and os.environ.get("GMPGR_ORDER", "cluster") != "bfs"):
+                from .locality import cluster_order
+
+                rows = self.rows if self.rows is not None else ids
+                if int(np.max(rows)) < len(items):
+                    order = cluster_order(items, slot_rows=rows, device=device)
+            h = _lib.DeviceGraph(layers, levels, entry, ids, rows=self.rows, device=device, order=order)
             self._dev[device] = h
         return h

@@ -233,7 +233,7 @@ def c_hipanns_batch(index: GraphIndex, model, users, item_embeddings,
     dm = metric.device_model(device)
     if users.shape[1] != dm.d_h:
         raise InvalidArgumentError(f"user embedding dim {users.shape[1]} != d_h {dm.d_h}")
-    g = index.device_graph(device)
+    g = index.device_graph(device, items=item_embeddings)
     it = device_items(item_embeddings, device)
     if it.d != dm.d_h:
         raise InvalidArgumentError("item embedding dim != model d_h")

@@ -148,3 +148,15 @@ def test_cfg1_graph_identical_to_reference_build():
     idx = P.GraphIndex.build(emb.astype(np.float64), m=16, ef_construction=64, seed=0)
     assert workload.graph_digest(idx) == str(z["graph_sha256"])
     assert idx.layer_node_counts() == list(z["layer_counts"])
+
+
+def test_parallel_build_equals_single_thread(monkeypatch):
+    """The speculative parallel build (planners + in-order committer) is exact: any thread
+    count gives the sequential graph."""
+    vectors = clustered(20_000, 16, seed=11, n_clusters=64)
+    graphs = []
+    for threads in ("1", "3", "8"):
+        monkeypatch.setenv("GMPGR_BUILD_THREADS", threads)
+        idx = P.GraphIndex.build(vectors, m=8, ef_construction=32, seed=2)
+        graphs.append(workload.graph_digest(idx))
+    assert graphs[0] == graphs[1] == graphs[2]

@@ -32,7 +32,7 @@ def main():
     torch.cuda.set_device(0)
     wl = workload.make(cfg, n_queries=nq)
     dm = wl.model.metric.device_model(0)
-    g = wl.index.device_graph(0)
+    g = wl.index.device_graph(0, items=wl.items)
     it = _lib.DeviceItems(wl.items, 0)
     s = _lib.DeviceSearcher(0)
     Q, k, L = nq, kw["k"], g.n_layers

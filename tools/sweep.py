@@ -28,7 +28,7 @@ def main():
     wl = workload.make("cfg5", n_queries=Qmax)
     print(f"built in {wl.build_s:.1f}s layers {wl.index.layer_node_counts()}", flush=True)
     dm = wl.model.metric.device_model(0)
-    g = wl.index.device_graph(0)
+    g = wl.index.device_graph(0, items=wl.items)
     it = _lib.DeviceItems(wl.items, 0)
     s = _lib.DeviceSearcher(0)
     users = torch.from_numpy(wl.users).cuda()
