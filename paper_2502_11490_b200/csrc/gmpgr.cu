@@ -1017,7 +1017,7 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
 size_t duo_unit_bytes(int64_t G, int64_t capF, int64_t capS, int64_t capP, int64_t hcap, int64_t vwords,
                       int64_t logcap) {
     const int64_t lF = capF * G, lS = capS * G;
-    return (size_t)(2 * 2 * lF * 4 + 7 * lS * 4 + 2 * lS * 8 + hcap * 8 + G * 2 * capP * 16 + G * vwords * 4 +
+    return (size_t)(2 * 2 * lF * 4 + 5 * lS * 4 + 2 * lS * 8 + hcap * 8 + G * 2 * capP * 16 + G * vwords * 4 +
                     G * logcap * 4);
 }
 
@@ -1032,7 +1032,7 @@ int ensure_duo_scratch(gr_searcher *S, int64_t units, int64_t G, int64_t capF, i
     int rc = GR_OK;
     if ((rc = dmalloc(&D.f_slot, (size_t)units * 2 * lF))) return rc;
     if ((rc = dmalloc(&D.f_srch, (size_t)units * 2 * lF))) return rc;
-    int32_t **lists[] = {&D.surv_v, &D.surv_i, &D.cont_v, &D.cont_i, &D.fr_v, &D.fr_i, &D.seg_v};
+    int32_t **lists[] = {&D.surv_v, &D.surv_i, &D.cont_v, &D.cont_i, &D.seg_v};
     for (int32_t **l : lists)
         if ((rc = dmalloc(l, (size_t)units * lS))) return rc;
     if ((rc = dmalloc(&D.fr_key, (size_t)units * lS))) return rc;
@@ -1194,8 +1194,6 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     a.surv_i = D.surv_i;
     a.cont_v = D.cont_v;
     a.cont_i = D.cont_i;
-    a.fr_v = D.fr_v;
-    a.fr_i = D.fr_i;
     a.fr_key = D.fr_key;
     a.seg_v = D.seg_v;
     a.seg_key = D.seg_key;

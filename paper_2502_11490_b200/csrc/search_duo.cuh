@@ -123,6 +123,17 @@ struct ExactU {
     }
 };
 
+// warp-aggregated append of v when ok
+__device__ __forceinline__ void warp_append1(bool ok, int32_t v, int *counter, int32_t *dv) {
+    const int lane = threadIdx.x & 31;
+    const unsigned mask = __ballot_sync(0xffffffffu, ok);
+    if (!mask) return;
+    int base = 0;
+    if (lane == 0) base = atomicAdd(counter, __popc(mask));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    if (ok) dv[base + __popc(mask & ((1u << lane) - 1u))] = v;
+}
+
 // (query slot, node) -> survivor index hash entries: key = gq << 31 | v (35 bits), t < 2^24
 #define GR_HASH_EMPTY 0xFFFFFFFFFFFFFFFFull
 __device__ __forceinline__ uint32_t duo_hash(uint64_t key) {
@@ -141,10 +152,14 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     __shared__ MqState<G> sts[2];
     __shared__ unsigned long long ph_acc[16];
     __shared__ unsigned bc[2];  // tensor-core band certificate (band_record)
-    __shared__ int nC_[2], nlog_[2][G];
+    __shared__ int nC_[2], nlog_[2][G], hs_[2], ovf_[2];
     const int tid = threadIdx.x, unit = tid >> 8, lt = tid & 255, warp = lt >> 5, lane = lt & 31;
     if (tid < 16) ph_acc[tid] = 0;
-    if (tid < 2) bc[tid] = 0u;
+    if (tid < 2) {
+        bc[tid] = 0u;
+        hs_[tid] = 4096;  // survivor hash size in use (grows with the survivor counts seen)
+        ovf_[tid] = 0;
+    }
     const DevModel &M = a.M;
     const DevGraph &g = a.g;
     auto usync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + unit) : "memory"); };
@@ -212,13 +227,15 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     int32_t *fsrch[2] = {a.f_srch + ug * 2 * capF, a.f_srch + ug * 2 * capF + capF};
     int32_t *surv_v = a.surv_v + ug * capS, *surv_i = a.surv_i + ug * capS;
     int32_t *cont_v = a.cont_v + ug * capS, *cont_i = a.cont_i + ug * capS;
-    int32_t *fr_v = a.fr_v + ug * capS, *fr_i = a.fr_i + ug * capS;
+    // fresh claims ARE the survivors (unique per (query, node)); their searcher field is
+    // lowered to the lowest toucher by the resolve pass before the frontier split reads it
+    int32_t *fr_v = surv_v, *fr_i = surv_i;
     uint64_t *fr_key = a.fr_key + ug * capS;
     int32_t *seg_v = a.seg_v + ug * capS;
     uint64_t *seg_key = a.seg_key + ug * capS;
     uint64_t *htab = a.hash + ug * a.hash_cap;
-    int32_t *rq = surv_v;    // re-score requests (gq << 24 | index)
-    int32_t *seg_ex = fr_i;  // after the scatter
+    int32_t *rq = cont_v;      // re-score requests (gq << 24 | index); contested lists are dead
+    int32_t *seg_ex = cont_i;  // after resolve
     auto vis_of = [&](int gq) { return a.vis + (ug * G + gq) * a.vis_words; };
     auto log_of = [&](int gq) { return a.vlog + (ug * G + gq) * (int64_t)a.log_cap; };
     auto pkey = [&](int gq, int c) { return a.pool_key + ((ug * G + gq) * 2 + c) * capP; };
@@ -372,7 +389,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 for (int i0 = 0; i0 < np; i0 += NTH) {
                     const int i = i0 + lt;
                     bool ok = i < np && !(pm[i] & 1) && pred(gq, orderable_f32((uint32_t)(pk[i] >> 32)));
-                    warp_append2(ok, (gq << 24) | i, 0, &st.nRq, rq, surv_i);
+                    warp_append1(ok, (gq << 24) | i, &st.nRq, rq);
                 }
             }
             usync();
@@ -422,56 +439,66 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             }
             usync();
         };
-        // owner resolution (lowest searcher) + claim (D bits) + visited log; survivors
-        // [0, nS) become fresh entries [base, base + nS)
+        // survivor hash insert (expand inserts as it reserves; resolve rebuilds on overflow)
+        auto hash_insert = [&](int32_t v, int32_t gi, int t, uint32_t hmask) {
+            const uint64_t key = ((uint64_t)(gi >> 16) << 31) | (uint64_t)v;
+            const uint64_t e = (key << 24) | (uint64_t)t;
+            uint32_t hh = duo_hash(key) & hmask;
+            while (atomicCAS(reinterpret_cast<unsigned long long *>(htab + hh), GR_HASH_EMPTY, e) != GR_HASH_EMPTY)
+                hh = (hh + 1) & hmask;
+        };
+        // owner resolution: every contested touch lowers its survivor's searcher code to the
+        // lowest toucher (atomicMin); every survivor is claimed (D bit) and logged.  The
+        // survivors [0, nS) are this hop's fresh claims.
         auto resolve = [&](int nS, int nCont) {
-            const int base = st.nFresh;
-            if (nCont > 0) {
-                int hs = 64;
-                while (hs < 2 * nS) hs <<= 1;
-                const uint32_t hmask = (uint32_t)hs - 1u;
-                for (int t = lt; t < nS; t += NTH) {
-                    const uint64_t key = ((uint64_t)(surv_i[t] >> 16) << 31) | (uint64_t)surv_v[t];
-                    const uint64_t e = (key << 24) | (uint64_t)t;
-                    uint32_t h = duo_hash(key) & hmask;
-                    while (atomicCAS(reinterpret_cast<unsigned long long *>(htab + h), GR_HASH_EMPTY, e) != GR_HASH_EMPTY)
-                        h = (h + 1) & hmask;
-                }
+            int hs = hs_[unit];
+            if (ovf_[unit]) {  // more survivors than the table admits: rebuild it bigger
+                int nh = hs;
+                while (nh < 2 * nS) nh <<= 1;
+                for (int h = lt; h < nh; h += NTH) htab[h] = GR_HASH_EMPTY;
                 usync();
-                for (int c = lt; c < nCont; c += NTH) {
-                    const int32_t v = cont_v[c], gi = cont_i[c];
-                    const uint64_t key = ((uint64_t)(gi >> 16) << 31) | (uint64_t)v;
-                    uint32_t h = duo_hash(key) & hmask;
-                    for (;;) {
-                        const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long *>(htab + h));
-                        if ((e >> 24) == key) {
-                            atomicMin(surv_i + (int)(e & 0xFFFFFF), gi);
-                            break;
-                        }
-                        if (e == GR_HASH_EMPTY) break;  // unreachable: the first toucher inserted it
-                        h = (h + 1) & hmask;
+                for (int t = lt; t < nS; t += NTH) hash_insert(surv_v[t], surv_i[t], t, (uint32_t)nh - 1u);
+                usync();
+                hs = nh;
+            }
+            const uint32_t hmask = (uint32_t)hs - 1u;
+            for (int c = lt; c < nCont; c += NTH) {
+                const int32_t v = cont_v[c], gi = cont_i[c];
+                const uint64_t key = ((uint64_t)(gi >> 16) << 31) | (uint64_t)v;
+                uint32_t hh = duo_hash(key) & hmask;
+                for (;;) {
+                    const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long *>(htab + hh));
+                    if ((e >> 24) == key) {
+                        atomicMin(surv_i + (int)(e & 0xFFFFFF), gi);
+                        break;
                     }
+                    if (e == GR_HASH_EMPTY) break;  // unreachable: the first toucher inserted it
+                    hh = (hh + 1) & hmask;
                 }
-                usync();
-                for (int h = lt; h < hs; h += NTH) htab[h] = GR_HASH_EMPTY;
             }
             for (int t0 = 0; t0 < nS; t0 += NTH) {
                 const int t = t0 + lt;
                 const bool ok = t < nS;
-                int32_t v = 0, gi = 0;
+                int32_t v = 0, gq = 0;
                 if (ok) {
                     v = surv_v[t];
-                    gi = __ldcg(surv_i + t);
-                    fr_v[base + t] = v;
-                    fr_i[base + t] = gi;
-                    atomicOr(vis_of(gi >> 16) + (v >> 4), 1u << (2 * (v & 15)));
+                    gq = surv_i[t] >> 16;  // the query never changes, only the searcher
+                    atomicOr(vis_of(gq) + (v >> 4), 1u << (2 * (v & 15)));
                 }
-                const int gq = gi >> 16;
                 const int li = warp_append(gq, ok, [&](int q) { return &nlog[q]; });
                 if (ok && li < a.log_cap) log_of(gq)[li] = v;
             }
             usync();
-            if (lt == 0) st.nFresh = base + nS;
+            // the table is idle until the next hop's expand: clear the used part, size it for
+            // the survivor count just seen
+            for (int h = lt; h < hs; h += NTH) htab[h] = GR_HASH_EMPTY;
+            if (lt == 0) {
+                st.nFresh = nS;
+                int nh = hs;
+                while (nh < 2 * nS && (int64_t)nh * 2 <= a.hash_cap) nh <<= 1;
+                hs_[unit] = nh;
+                ovf_[unit] = 0;
+            }
             usync();
         };
         auto sort_pools = [&]() {
@@ -485,16 +512,15 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             usync();
         };
 
-        // ================= init: entry + its top-layer neighbourhood (hop 0)
+        // ================= init: entry + its top-layer neighbourhood (hop 0), as first
+        // touches of searcher 0 (the entry's row never contains the entry)
         if (lt == 0) { st.nS = 0; st.nFresh = 0; nC = 0; }
         usync();
         if (lt < G && st.qs[lt].q >= 0) {
-            const int idx = atomicAdd(&st.nFresh, 1);
-            atomicOr(vis_of(lt) + (g.entry >> 4), 3u << (2 * (g.entry & 15)));
-            fr_v[idx] = g.entry;
-            fr_i[idx] = lt << 16;
-            const int li = atomicAdd(&nlog[lt], 1);
-            if (li < a.log_cap) log_of(lt)[li] = g.entry;
+            const int idx = atomicAdd(&st.nS, 1);
+            atomicOr(vis_of(lt) + (g.entry >> 4), 2u << (2 * (g.entry & 15)));
+            surv_v[idx] = g.entry;
+            surv_i[idx] = lt << 16;
         }
         usync();
         if (warp < G && st.qs[warp].q >= 0) {
@@ -514,6 +540,13 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             }
         }
         usync();
+        if (nC > 0 || st.nS * 2 > hs_[unit]) {  // contested (not expected here) or big: (re)build
+            if (lt == 0) ovf_[unit] = 1;
+            usync();
+        } else {
+            for (int t = lt; t < st.nS; t += NTH) hash_insert(surv_v[t], surv_i[t], t, (uint32_t)hs_[unit] - 1u);
+            usync();
+        }
         resolve(st.nS, nC);
         score_fresh(st.nFresh, top, 0);
         compact_pools();
@@ -567,6 +600,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 const int fc = st.f_cur;
                 if (lt == 0) { st.nS = 0; st.nFresh = 0; nC = 0; }
                 usync();
+                const int hs_now = hs_[unit];
                 // ---- expand + claim: a warp takes RW frontier rows and spreads their 16-byte
                 // pieces over its lanes (<= 3 per lane): every row load in flight at once, then
                 // every claim atomic, then one aggregated reservation per list per warp;
@@ -644,7 +678,15 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                if (vv[u] >= 0 && s2[j][u] == 0u) { surv_v[bs] = vv[u]; surv_i[bs] = pgi[j]; ++bs; }
+                                if (vv[u] >= 0 && s2[j][u] == 0u) {
+                                    surv_v[bs] = vv[u];
+                                    surv_i[bs] = pgi[j];
+                                    // the survivor goes into the (query, node) hash now, under the
+                                    // other atomics' latency; a table over half full is rebuilt by resolve
+                                    if (2 * bs < hs_now) hash_insert(vv[u], pgi[j], bs, (uint32_t)hs_now - 1u);
+                                    else ovf_[unit] = 1;
+                                    ++bs;
+                                }
                                 if (vv[u] >= 0 && s2[j][u] == 2u) { cont_v[bcn] = vv[u]; cont_i[bcn] = pgi[j]; ++bcn; }
                             }
                         }
@@ -728,7 +770,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const int j = j0 + lane;
                             const bool in = j < ni &&
                                 fabsf(orderable_f32((uint32_t)(seg_key[off + j] >> 32)) - Ts) <= bd;
-                            warp_append2(in, (gq << 24) | (off + j), 0, &st.nRq, rq, surv_i);
+                            warp_append1(in, (gq << 24) | (off + j), &st.nRq, rq);
                         }
                     }
                     usync();
