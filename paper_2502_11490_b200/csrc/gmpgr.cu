@@ -1037,13 +1037,13 @@ int ensure_duo_scratch(gr_searcher *S, int64_t units, int64_t G, int64_t capF, i
         if ((rc = dmalloc(l, (size_t)units * lS))) return rc;
     if ((rc = dmalloc(&D.fr_key, (size_t)units * lS))) return rc;
     if ((rc = dmalloc(&D.seg_key, (size_t)units * lS))) return rc;
-    if ((rc = dmalloc(&D.hash, (size_t)units * hcap))) return rc;
+    if (hcap && (rc = dmalloc(&D.hash, (size_t)units * hcap))) return rc;
     if ((rc = dmalloc(&D.pool_key, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&D.pool_slot, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&D.pool_meta, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&D.vis, (size_t)slots * vwords))) return rc;
     if ((rc = dmalloc(&D.vlog, (size_t)slots * logcap))) return rc;
-    GR_CUDA(cudaMemset(D.hash, 0xFF, (size_t)units * hcap * 8));
+    if (hcap) GR_CUDA(cudaMemset(D.hash, 0xFF, (size_t)units * hcap * 8));
     GR_CUDA(cudaMemset(D.vis, 0, (size_t)slots * vwords * 4));
     D.units = units;
     D.G = G;
@@ -1131,8 +1131,7 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
                                            G->max_deg + 1) + 64;
     const int64_t capP = p->k + capS;
     if (capS * GQ >= (1 << 24) || capP >= (1 << 24)) return -1;
-    int64_t hcap = 64;
-    while (hcap < 2 * capS * GQ) hcap <<= 1;
+    const int64_t hcap = 0;  // (query, node) hash: not needed (the first toucher is the owner)
     const int64_t vwords = (G->dg.n + 15) / 16;
     const int64_t logcap = std::min<int64_t>(G->dg.n + 1, 1 << 16);
     if (int rc = set_smem(kern, smem)) return rc;

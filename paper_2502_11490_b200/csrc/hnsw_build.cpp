@@ -500,6 +500,18 @@ struct Builder {
     }
 
     // the write half of insert: connects in the reference's order, entry update
+    // start every row a commit of P will touch (the committer calls it one plan ahead too)
+    void prefetch_rows(const Plan &P, int32_t top) const {
+        for (int l = std::min(P.level, (int)top); l >= 0; --l)
+            for (int64_t nb : P.kept[l]) {
+                const int64_t rb = nb * (int64_t)cap_of(l);
+                __builtin_prefetch(cnts[l] + nb, 1);
+                __builtin_prefetch(nbrs[l] + rb, 1);
+                for (int b = 0; b < cap_of(l) * 8; b += 64)
+                    __builtin_prefetch(reinterpret_cast<const char *>(rowd[l].p + rb) + b, 1);
+            }
+    }
+
     void commit(const Plan &P, int32_t &entry, int32_t &top) {
         cur = P.slot;
         modlog[cur % MR].clear();
@@ -513,14 +525,7 @@ struct Builder {
             return;
         }
         const int l0 = std::min(P.level, (int)top);
-        for (int l = l0; l >= 0; --l)  // start every row this commit will touch
-            for (int64_t nb : P.kept[l]) {
-                const int64_t rb = nb * (int64_t)cap_of(l);
-                __builtin_prefetch(cnts[l] + nb, 1);
-                __builtin_prefetch(nbrs[l] + rb, 1);
-                for (int b = 0; b < cap_of(l) * 8; b += 64)
-                    __builtin_prefetch(reinterpret_cast<const char *>(rowd[l].p + rb) + b, 1);
-            }
+        prefetch_rows(P, top);
         for (int l = l0; l >= 0; --l)
             for (size_t j = 0; j < P.kept[l].size(); ++j) connect(l, P.slot, P.kept[l][j], P.kept_d[l][j]);
         if (P.level > top) {
@@ -692,6 +697,8 @@ extern "C" int gr_hnsw_insert(int64_t n0, int64_t n1, int32_t dim, const double 
             P.base = s;
         }
         const auto tc0 = std::chrono::steady_clock::now();
+        if (T > 1 && s + 1 < n1 && ready[(s + 1) % R].load(std::memory_order_acquire) == s + 1)
+            B.prefetch_rows(plans[(s + 1) % R], top);  // next commit's rows, one commit ahead
         if (!B.still_exact(P, s, entry, top)) {
             B.plan(ctx[0], s, entry, top, P);
             ++replans;

@@ -9,14 +9,15 @@
 //
 // Visited state (claims) -- bounded by N/4 bytes per resident query, not 4N:
 //   two bits per node per query slot: D = claimed before this hop, T = touched this hop.
-//   expand:  old = atomicOr(word, T)  ->  D set: already claimed, drop;  T set: contested
-//            (another searcher touched it first this hop);  else: first touch -> survivor.
-//   resolve: owner(v) = the LOWEST searcher listing v (the reference's lock-step claim order,
-//            search.py:220-224, 261-265): survivors go into a per-unit open-addressing hash
-//            ((query, node) -> survivor index), every contested entry does atomicMin of its
-//            searcher code on its survivor; every survivor is fresh, D is set, the node is
-//            logged; at query end the logged nodes' words are zeroed (or the slot's whole
-//            bitset when the log overflowed).
+//   expand:  warp w of a unit owns query w and walks that query's frontier in list order
+//            (searcher-ascending, search.py:261-265) in batches that never span two searchers;
+//            a batch's claim atomics have all returned before the next batch issues its own.
+//            old = atomicOr(word, T):  D set -> already claimed;  T set -> touched earlier
+//            this hop by the same or a LOWER searcher;  neither -> first touch.  So the first
+//            toucher is the lowest searcher listing the node -- the reference's lock-step
+//            ownership (search.py:220-224) -- with no second resolution pass.
+//   claim:   every first touch is fresh; D is set and the node is logged; at query end the
+//            logged nodes' words are zeroed (or the slot's whole bitset when the log overflowed).
 // MODE 0: exact-fp32 scoring of every claim (32-pair tiles per unit, weights in shared memory).
 // MODE 1: tcgen05 split-bf16 scoring of 128-pair tiles (tc_pipe2.cuh) + exact re-scoring of
 //         the band around every selection threshold, with the run-time band certificate.
@@ -134,16 +135,10 @@ __device__ __forceinline__ void warp_append1(bool ok, int32_t v, int *counter, i
     if (ok) dv[base + __popc(mask & ((1u << lane) - 1u))] = v;
 }
 
-// (query slot, node) -> survivor index hash entries: key = gq << 31 | v (35 bits), t < 2^24
-#define GR_HASH_EMPTY 0xFFFFFFFFFFFFFFFFull
-__device__ __forceinline__ uint32_t duo_hash(uint64_t key) {
-    return (uint32_t)((key * 0x9E3779B97F4A7C15ull) >> 32);
-}
-
 template <int DH, int ZZ, int MODE, int G>
 __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_constant__ SearchArgs a) {
     constexpr int NTH = 256, NW = 8, GT = NTH / G;
-    static_assert(GT == 32, "one warp per query for the pool sorts");
+    static_assert(GT == 32 && NW == G, "one warp per query (pool sorts, expand)");
     using EX = ExactU<DH, ZZ>;
     using TP = TcPipe2<DH, ZZ>;
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -152,14 +147,10 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     __shared__ MqState<G> sts[2];
     __shared__ unsigned long long ph_acc[16];
     __shared__ unsigned bc[2];  // tensor-core band certificate (band_record)
-    __shared__ int nC_[2], nlog_[2][G], hs_[2], ovf_[2];
+    __shared__ int nlog_[2][G];
     const int tid = threadIdx.x, unit = tid >> 8, lt = tid & 255, warp = lt >> 5, lane = lt & 31;
     if (tid < 16) ph_acc[tid] = 0;
-    if (tid < 2) {
-        bc[tid] = 0u;
-        hs_[tid] = 4096;  // survivor hash size in use (grows with the survivor counts seen)
-        ovf_[tid] = 0;
-    }
+    if (tid < 2) bc[tid] = 0u;
     const DevModel &M = a.M;
     const DevGraph &g = a.g;
     auto usync = [&]() { asm volatile("bar.sync %0, 256;" ::"r"(1 + unit) : "memory"); };
@@ -218,7 +209,6 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     if constexpr (MODE == 1) tmem = *tptr + unit * TP::COLS;
 
     MqState<G> &st = sts[unit];
-    int &nC = nC_[unit];
     int *nlog = nlog_[unit];
     // ---- scratch: unit-level flattened lists, per-query visited bitsets / logs / pools
     const int64_t ug = (int64_t)blockIdx.x * 2 + unit;  // global unit index
@@ -233,7 +223,6 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     uint64_t *fr_key = a.fr_key + ug * capS;
     int32_t *seg_v = a.seg_v + ug * capS;
     uint64_t *seg_key = a.seg_key + ug * capS;
-    uint64_t *htab = a.hash + ug * a.hash_cap;
     int32_t *rq = cont_v;      // re-score requests (gq << 24 | index); contested lists are dead
     int32_t *seg_ex = cont_i;  // after resolve
     auto vis_of = [&](int gq) { return a.vis + (ug * G + gq) * a.vis_words; };
@@ -439,66 +428,22 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             }
             usync();
         };
-        // survivor hash insert (expand inserts as it reserves; resolve rebuilds on overflow)
-        auto hash_insert = [&](int32_t v, int32_t gi, int t, uint32_t hmask) {
-            const uint64_t key = ((uint64_t)(gi >> 16) << 31) | (uint64_t)v;
-            const uint64_t e = (key << 24) | (uint64_t)t;
-            uint32_t hh = duo_hash(key) & hmask;
-            while (atomicCAS(reinterpret_cast<unsigned long long *>(htab + hh), GR_HASH_EMPTY, e) != GR_HASH_EMPTY)
-                hh = (hh + 1) & hmask;
-        };
-        // owner resolution: every contested touch lowers its survivor's searcher code to the
-        // lowest toucher (atomicMin); every survivor is claimed (D bit) and logged.  The
-        // survivors [0, nS) are this hop's fresh claims.
-        auto resolve = [&](int nS, int nCont) {
-            int hs = hs_[unit];
-            if (ovf_[unit]) {  // more survivors than the table admits: rebuild it bigger
-                int nh = hs;
-                while (nh < 2 * nS) nh <<= 1;
-                for (int h = lt; h < nh; h += NTH) htab[h] = GR_HASH_EMPTY;
-                usync();
-                for (int t = lt; t < nS; t += NTH) hash_insert(surv_v[t], surv_i[t], t, (uint32_t)nh - 1u);
-                usync();
-                hs = nh;
-            }
-            const uint32_t hmask = (uint32_t)hs - 1u;
-            for (int c = lt; c < nCont; c += NTH) {
-                const int32_t v = cont_v[c], gi = cont_i[c];
-                const uint64_t key = ((uint64_t)(gi >> 16) << 31) | (uint64_t)v;
-                uint32_t hh = duo_hash(key) & hmask;
-                for (;;) {
-                    const uint64_t e = __ldcg(reinterpret_cast<const unsigned long long *>(htab + hh));
-                    if ((e >> 24) == key) {
-                        atomicMin(surv_i + (int)(e & 0xFFFFFF), gi);
-                        break;
-                    }
-                    if (e == GR_HASH_EMPTY) break;  // unreachable: the first toucher inserted it
-                    hh = (hh + 1) & hmask;
-                }
-            }
+        // claim this hop's first touches [0, nS) (= the fresh claims): D bit + visited log
+        auto resolve = [&](int nS) {
             for (int t0 = 0; t0 < nS; t0 += NTH) {
                 const int t = t0 + lt;
                 const bool ok = t < nS;
                 int32_t v = 0, gq = 0;
                 if (ok) {
                     v = surv_v[t];
-                    gq = surv_i[t] >> 16;  // the query never changes, only the searcher
+                    gq = surv_i[t] >> 16;
                     atomicOr(vis_of(gq) + (v >> 4), 1u << (2 * (v & 15)));
                 }
                 const int li = warp_append(gq, ok, [&](int q) { return &nlog[q]; });
                 if (ok && li < a.log_cap) log_of(gq)[li] = v;
             }
             usync();
-            // the table is idle until the next hop's expand: clear the used part, size it for
-            // the survivor count just seen
-            for (int h = lt; h < hs; h += NTH) htab[h] = GR_HASH_EMPTY;
-            if (lt == 0) {
-                st.nFresh = nS;
-                int nh = hs;
-                while (nh < 2 * nS && (int64_t)nh * 2 <= a.hash_cap) nh <<= 1;
-                hs_[unit] = nh;
-                ovf_[unit] = 0;
-            }
+            if (lt == 0) st.nFresh = nS;
             usync();
         };
         auto sort_pools = [&]() {
@@ -514,7 +459,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
 
         // ================= init: entry + its top-layer neighbourhood (hop 0), as first
         // touches of searcher 0 (the entry's row never contains the entry)
-        if (lt == 0) { st.nS = 0; st.nFresh = 0; nC = 0; }
+        if (lt == 0) { st.nS = 0; st.nFresh = 0; }
         usync();
         if (lt < G && st.qs[lt].q >= 0) {
             const int idx = atomicAdd(&st.nS, 1);
@@ -535,19 +480,11 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     uint32_t s2 = 1u;
                     if (v >= 0) s2 = (atomicOr(vb + (v >> 4), 2u << (2 * (v & 15))) >> (2 * (v & 15))) & 3u;
                     warp_append2(v >= 0 && s2 == 0u, v, warp << 16, &st.nS, surv_v, surv_i);
-                    warp_append2(v >= 0 && s2 == 2u, v, warp << 16, &nC, cont_v, cont_i);
                 }
             }
         }
         usync();
-        if (nC > 0 || st.nS * 2 > hs_[unit]) {  // contested (not expected here) or big: (re)build
-            if (lt == 0) ovf_[unit] = 1;
-            usync();
-        } else {
-            for (int t = lt; t < st.nS; t += NTH) hash_insert(surv_v[t], surv_i[t], t, (uint32_t)hs_[unit] - 1u);
-            usync();
-        }
-        resolve(st.nS, nC);
+        resolve(st.nS);
         score_fresh(st.nFresh, top, 0);
         compact_pools();
         GR_PH(0);
@@ -598,56 +535,62 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 const int nF = st.nF;
                 if (nF == 0) { h += a.hops - 1 - t; break; }
                 const int fc = st.f_cur;
-                if (lt == 0) { st.nS = 0; st.nFresh = 0; nC = 0; }
+                if (lt == 0) { st.nS = 0; st.nFresh = 0; }
                 usync();
-                const int hs_now = hs_[unit];
-                // ---- expand + claim: a warp takes RW frontier rows and spreads their 16-byte
-                // pieces over its lanes (<= 3 per lane): every row load in flight at once, then
-                // every claim atomic, then one aggregated reservation per list per warp;
-                // software-pipelined (next batch's frontier entries and rows under this
-                // batch's atomics)
-                {
+                // ---- expand + claim: warp w owns query w and walks its frontier in list order
+                // (searcher-ascending) in batches of <= RW rows of ONE searcher; a batch's 16-byte
+                // row pieces are spread over the lanes (<= 3 per lane), all row loads in flight,
+                // then all claim atomics, then one survivor reservation.  Software-pipelined: the
+                // next batch's frontier entries and rows are fetched under this batch's atomics,
+                // whose results are consumed before the next batch issues its own.
+                if (st.qs[warp].q >= 0) {
                     const int P = g.ld[layer] >> 2;
                     const int RW = min(32, 96 / P), NP = RW * P;
                     constexpr unsigned FULL = 0xffffffffu;
-                    auto meta = [&](int e0, int32_t &ms, int32_t &mgi) {
+                    const int qend = st.qs[warp].f_off + st.qs[warp].f_cnt;
+                    uint32_t *vb = vis_of(warp);
+                    auto meta = [&](int e0, int32_t &ms, int &len) {
                         ms = -1;
-                        mgi = 0;
-                        if (lane < RW && e0 + lane < nF) { ms = fslot[fc][e0 + lane]; mgi = fsrch[fc][e0 + lane]; }
+                        int32_t mgi = 0;
+                        const bool in = lane < RW && e0 + lane < qend;
+                        if (in) { ms = fslot[fc][e0 + lane]; mgi = fsrch[fc][e0 + lane]; }
+                        const bool same = in && mgi == __shfl_sync(FULL, mgi, 0);
+                        len = __popc(__ballot_sync(FULL, same));  // a prefix: entries sorted by searcher
+                        if (!same) ms = -1;
+                        return __shfl_sync(FULL, mgi, 0);
                     };
-                    auto pieces = [&](int32_t ms, int32_t mgi, int4 (&pv)[3], int (&pgi)[3]) {
+                    auto pieces = [&](int32_t ms, int4 (&pv)[3]) {
                         const int4 *mrow = ms >= 0 ? reinterpret_cast<const int4 *>(graph_row(g, layer, ms)) : nullptr;
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const int pc = lane + 32 * j, r = min(pc / P, 31), c = pc - r * P;
                             const int4 *rp = reinterpret_cast<const int4 *>(
                                 __shfl_sync(FULL, reinterpret_cast<unsigned long long>(mrow), r));
-                            pgi[j] = __shfl_sync(FULL, mgi, r);
                             pv[j] = (pc < NP && rp) ? __ldg(rp + c) : make_int4(-1, -1, -1, -1);
                         }
                     };
-                    int32_t ms, mgi;
+                    int32_t ms;
+                    int len;
                     int4 pv[3];
-                    int pgi[3];
-                    int e0 = warp * RW;
-                    meta(e0, ms, mgi);
-                    pieces(ms, mgi, pv, pgi);
-                    for (; e0 < nF; e0 += NW * RW) {
-                        int32_t ms1, mgi1;
-                        meta(e0 + NW * RW, ms1, mgi1);
+                    int e0 = st.qs[warp].f_off;
+                    int32_t gi = meta(e0, ms, len);
+                    pieces(ms, pv);
+                    int nrows = 0, nnbr = 0;
+                    while (len > 0) {
+                        int32_t ms1;
+                        int len1;
+                        const int32_t gi1 = meta(e0 + len, ms1, len1);
                         uint32_t s2[3][4];  // 2-bit states before this touch (bit0 D, bit1 T)
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
-                            uint32_t *vb = vis_of(pgi[j] >> 16);
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
                                 s2[j][u] = vv[u] >= 0 ? atomicOr(vb + (vv[u] >> 4), 2u << (2 * (vv[u] & 15))) : 1u;
                         }
                         int4 pv1[3];
-                        int pgi1[3];
-                        pieces(ms1, mgi1, pv1, pgi1);
-                        int cs = 0, cc = 0, nv = 0;
+                        pieces(ms1, pv1);
+                        int cs = 0, nv = 0;
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
@@ -656,63 +599,40 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                                 if (vv[u] >= 0) s2[j][u] = (s2[j][u] >> (2 * (vv[u] & 15))) & 3u;
                                 nv += vv[u] >= 0;
                                 cs += s2[j][u] == 0u;
-                                cc += s2[j][u] == 2u;
                             }
                         }
-                        // one reservation per list per warp (inclusive scans of the lane counts)
-                        int is = cs, ic = cc;
+                        int is = cs;  // one reservation per warp (inclusive scan of the lane counts)
 #pragma unroll
                         for (int o = 1; o < 32; o <<= 1) {
-                            const int ys = __shfl_up_sync(FULL, is, o), yc = __shfl_up_sync(FULL, ic, o);
-                            if (lane >= o) { is += ys; ic += yc; }
+                            const int ys = __shfl_up_sync(FULL, is, o);
+                            if (lane >= o) is += ys;
                         }
-                        int bs = 0, bcn = 0;
-                        if (lane == 31) {
-                            if (is) bs = atomicAdd(&st.nS, is);
-                            if (ic) bcn = atomicAdd(&nC, ic);
-                        }
+                        int bs = 0;
+                        if (lane == 31 && is) bs = atomicAdd(&st.nS, is);
                         bs = __shfl_sync(FULL, bs, 31) + is - cs;
-                        bcn = __shfl_sync(FULL, bcn, 31) + ic - cc;
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
-                            for (int u = 0; u < 4; ++u) {
-                                if (vv[u] >= 0 && s2[j][u] == 0u) {
-                                    surv_v[bs] = vv[u];
-                                    surv_i[bs] = pgi[j];
-                                    // the survivor goes into the (query, node) hash now, under the
-                                    // other atomics' latency; a table over half full is rebuilt by resolve
-                                    if (2 * bs < hs_now) hash_insert(vv[u], pgi[j], bs, (uint32_t)hs_now - 1u);
-                                    else ovf_[unit] = 1;
-                                    ++bs;
-                                }
-                                if (vv[u] >= 0 && s2[j][u] == 2u) { cont_v[bcn] = vv[u]; cont_i[bcn] = pgi[j]; ++bcn; }
-                            }
+                            for (int u = 0; u < 4; ++u)
+                                if (vv[u] >= 0 && s2[j][u] == 0u) { surv_v[bs] = vv[u]; surv_i[bs] = gi; ++bs; }
                         }
-                        const int gq0 = __shfl_sync(FULL, mgi, 0) >> 16;
-                        if (__all_sync(FULL, ms < 0 || (mgi >> 16) == gq0)) {
-                            int nrow = __popc(__ballot_sync(FULL, ms >= 0)), tot = nv;
-#pragma unroll
-                            for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(FULL, tot, o);
-                            if (lane == 0) { atomicAdd(&st.qs[gq0].rows, nrow); atomicAdd(&st.qs[gq0].nbrs, tot); }
-                        } else {
-                            if (ms >= 0) atomicAdd(&st.qs[mgi >> 16].rows, 1);
-#pragma unroll
-                            for (int j = 0; j < 3; ++j) {
-                                const int n4 = (pv[j].x >= 0) + (pv[j].y >= 0) + (pv[j].z >= 0) + (pv[j].w >= 0);
-                                if (n4) atomicAdd(&st.qs[pgi[j] >> 16].nbrs, n4);
-                            }
-                        }
+                        nrows += len;
+                        nnbr += nv;
+                        e0 += len;
                         ms = ms1;
-                        mgi = mgi1;
+                        len = len1;
+                        gi = gi1;
 #pragma unroll
-                        for (int j = 0; j < 3; ++j) { pv[j] = pv1[j]; pgi[j] = pgi1[j]; }
+                        for (int j = 0; j < 3; ++j) pv[j] = pv1[j];
                     }
+#pragma unroll
+                    for (int o = 16; o > 0; o >>= 1) nnbr += __shfl_xor_sync(FULL, nnbr, o);
+                    if (lane == 0) { st.qs[warp].rows += nrows; st.qs[warp].nbrs += nnbr; }
                 }
                 usync();
                 GR_PH(2);
-                resolve(st.nS, nC);
+                resolve(st.nS);
                 GR_PH(3);
                 const int nFresh = st.nFresh;
                 score_fresh(nFresh, layer, h);
@@ -747,7 +667,13 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         acc += __shfl_sync(0xffffffffu, x, 31);
                         accf += __shfl_sync(0xffffffffu, xf, 31);
                     }
+                    __syncwarp();
                     if (lane == 0) st.nFn = accf;
+                    if (lane < G) {  // each query's next frontier range (its segments are contiguous)
+                        const int lo = fn_off[lane * a.kp], hi = lane + 1 < G ? fn_off[(lane + 1) * a.kp] : accf;
+                        st.qs[lane].f_off = lo;
+                        st.qs[lane].f_cnt = hi - lo;
+                    }
                 }
                 usync();
                 for (int t2 = lt; t2 < nFresh; t2 += NTH) {
