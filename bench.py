@@ -190,7 +190,7 @@ def run_reference(args):
     if args.config in ("cfg1", "cfg2"):
         wl = workload.make_reference(args.config, device=None)
     else:
-        wl = workload.make(args.config, rank=0, device=local, host_items=True)
+        wl = workload.make(args.config, rank=0, device=local, host_items=True, graph=args.graph)
     log(f"[reference] workload {args.config} built in {wl.build_s:.1f}s")
     threads = host_threads()
     qps = cpu_probe(wl, threads)
@@ -237,6 +237,8 @@ def config_of(args, wl):
             "graph": ("reference GraphIndex.build(m=16, ef_construction=64, seed=0) on the "
                       "reference's clustered_vectors/create_model inputs, native exact build "
                       "(graph digest identical to the reference's)" if args.config in ("cfg1", "cfg2")
+                      else f"the reference's construction algorithm (GraphIndex.build m={wl.index.m}, "
+                           f"ef_construction=64; native exact parallel build)" if getattr(args, "graph", "gpu") == "exact"
                       else "GPU producer (builder.py): reference level draws + symmetric pruned k-NN")}
 
 
@@ -286,7 +288,7 @@ def run_gmpgr(args):
         # BASELINE configs 1/2 on the reference's own inputs and (native exact) graph build
         wl = workload.make_reference(args.config, device=dev)
     else:
-        wl = workload.make(args.config, rank=rank, device=dev, host_items=want_cpu)
+        wl = workload.make(args.config, rank=rank, device=dev, host_items=want_cpu, graph=args.graph)
     log(f"[rank {rank}] workload {args.config} built in {wl.build_s:.1f}s, "
         f"layers {wl.index.layer_node_counts()}")
     model, index = wl.model, wl.index
@@ -371,7 +373,8 @@ def run_gmpgr(args):
     achieved_gbs = bytes_launch / per_launch / 1e9
     sm_mhz = pk.get("sm_max_mhz", 1965.0)
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # separate fmul/fadd issue, TFLOP/s
-    kname = "hipanns_mq_kernel" if d_h in (64, 128) else "hipanns_search_kernel"
+    kname = ("hipanns_mq_kernel" if os.environ.get("GMPGR_KERNEL") == "mq" else "hipanns_duo_kernel") \
+        if d_h in (64, 128) else "hipanns_search_kernel"
     prof = ncu_profile(kname, per_launch, args.config, args.mode)
     traffic = tensor_ncu = None
     if prof:
@@ -594,6 +597,10 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--graph", default="gpu", choices=["gpu", "exact"],
+                    help="cfg3 graph: gpu = bulk GPU producer (builder.py, ~20 s); exact = the "
+                         "reference's own construction algorithm (native exact parallel build, "
+                         "minutes at 10M items)")
     ap.add_argument("--no-operating-points", dest="operating_points", action="store_false",
                     help="skip the extra kp=32/hops=10 (high-recall) operating point")
     ap.add_argument("--k-parallel", type=int, default=PARAMS["k_parallel"],

@@ -22,6 +22,8 @@
 // MODE 1: tcgen05 split-bf16 scoring of 128-pair tiles (tc_pipe2.cuh) + exact re-scoring of
 //         the band around every selection threshold, with the run-time band certificate.
 #pragma once
+#include <cstdio>
+
 #include "common.cuh"
 #include "search_kernel.cuh"
 #include "search_mq.cuh"
@@ -134,6 +136,23 @@ __device__ __forceinline__ void warp_append1(bool ok, int32_t v, int *counter, i
     base = __shfl_sync(0xffffffffu, base, 0);
     if (ok) dv[base + __popc(mask & ((1u << lane) - 1u))] = v;
 }
+
+// bounds checks for debugging builds (-DGR_DUO_DEBUG): report and trap
+#ifdef GR_DUO_DEBUG
+#define GR_DCHECK(cond, ...)                                  \
+    do {                                                      \
+        if (!(cond)) {                                        \
+            printf("GR_DCHECK %s:%d: ", __FILE__, __LINE__);  \
+            printf(__VA_ARGS__);                              \
+            printf("\n");                                    \
+            __trap();                                         \
+        }                                                     \
+    } while (0)
+#else
+#define GR_DCHECK(cond, ...) \
+    do {                     \
+    } while (0)
+#endif
 
 template <int DH, int ZZ, int MODE, int G>
 __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_constant__ SearchArgs a) {
@@ -437,6 +456,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 if (ok) {
                     v = surv_v[t];
                     gq = surv_i[t] >> 16;
+                    GR_DCHECK(gq >= 0 && gq < G && v >= 0 && v < g.n, "resolve t %d gq %d v %d", t, gq, v);
                     atomicOr(vis_of(gq) + (v >> 4), 1u << (2 * (v & 15)));
                 }
                 const int li = warp_append(gq, ok, [&](int q) { return &nlog[q]; });
@@ -553,11 +573,18 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         ms = -1;
                         int32_t mgi = 0;
                         const bool in = lane < RW && e0 + lane < qend;
-                        if (in) { ms = fslot[fc][e0 + lane]; mgi = fsrch[fc][e0 + lane]; }
-                        const bool same = in && mgi == __shfl_sync(FULL, mgi, 0);
+                        if (in) {
+                            GR_DCHECK(e0 + lane < capF, "fslot index %d >= %lld", e0 + lane, (long long)capF);
+                            ms = fslot[fc][e0 + lane];
+                            mgi = fsrch[fc][e0 + lane];
+                            GR_DCHECK(ms >= 0 && ms < g.n && (mgi >> 16) == warp, "frontier entry %d gi %x warp %d",
+                                      ms, mgi, warp);
+                        }
+                        const int32_t head = __shfl_sync(FULL, mgi, 0);  // every lane: no short circuit
+                        const bool same = in && mgi == head;
                         len = __popc(__ballot_sync(FULL, same));  // a prefix: entries sorted by searcher
                         if (!same) ms = -1;
-                        return __shfl_sync(FULL, mgi, 0);
+                        return head;
                     };
                     auto pieces = [&](int32_t ms, int4 (&pv)[3]) {
                         const int4 *mrow = ms >= 0 ? reinterpret_cast<const int4 *>(graph_row(g, layer, ms)) : nullptr;
@@ -615,7 +642,12 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
-                                if (vv[u] >= 0 && s2[j][u] == 0u) { surv_v[bs] = vv[u]; surv_i[bs] = gi; ++bs; }
+                                if (vv[u] >= 0 && s2[j][u] == 0u) {
+                                    GR_DCHECK(bs < capS && vv[u] < g.n, "survivor %d cap %lld v %d", bs, (long long)capS, vv[u]);
+                                    surv_v[bs] = vv[u];
+                                    surv_i[bs] = gi;
+                                    ++bs;
+                                }
                         }
                         nrows += len;
                         nnbr += nv;
@@ -707,6 +739,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     const int ni = seg_cnt[sg], off = seg_off[sg], fo = fn_off[sg];
                     const int gi = ((sg / a.kp) << 16) | (sg % a.kp);
                     if (ni <= a.ef) {
+                        GR_DCHECK(fo + ni <= capF, "frontier write %d + %d > %lld", fo, ni, (long long)capF);
                         for (int j = lane; j < ni; j += 32) { fslot[fn][fo + j] = seg_v[off + j]; fsrch[fn][fo + j] = gi; }
                     } else {
                         const uint64_t T = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);

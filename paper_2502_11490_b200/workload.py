@@ -95,7 +95,11 @@ def make_reference(name: str, device: int | None = 0, n_queries: int | None = No
 
 
 def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
-         n_queries: int | None = None, n_items: int | None = None) -> Workload:
+         n_queries: int | None = None, n_items: int | None = None, graph: str = "gpu") -> Workload:
+    """Synthetic workload of a BASELINE shape.  graph="gpu": bulk GPU producer (builder.py);
+    graph="exact": the reference's own sequential construction algorithm (native exact
+    parallel build, GraphIndex.build(method="exact"), m and ef_construction=64 as the
+    reference defaults) over the same items."""
     import torch
 
     N, d, m, C, Z, Q = CONFIGS[name]
@@ -122,7 +126,10 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     users = (torch.randn(Q, d, generator=gu, device=dev) @ w_user).cpu().numpy()
     torch.backends.cuda.matmul.allow_tf32 = prev
     del centers, assign
-    index = GraphIndex.build(items, m=m, seed=0, device=dev, method="gpu")
+    if graph == "exact":
+        index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
+    else:
+        index = GraphIndex.build(items, m=m, seed=0, device=dev, method="gpu")
     torch.cuda.synchronize(dev)
     torch.cuda.empty_cache()  # hand the builder's cached blocks back before the search scratch
     items_host = items.cpu().numpy() if host_items else None
