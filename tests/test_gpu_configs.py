@@ -257,3 +257,24 @@ def test_sharded_world1_nccl_equals_per_shard_pool_merge(P):
     p.start()
     p.join(timeout=600)
     assert q.get(timeout=5) == "ok"
+
+
+def test_failed_call_leaves_the_searcher_usable(P, monkeypatch):
+    """SURVEY §5 failure isolation: a call that fails (allocation over the scratch budget,
+    a contract violation) fails alone -- the next call on the same handles returns the
+    reference's results."""
+    from paper_2502_11490_b200 import _lib
+
+    z, model, emb, users, idx = reference_workload(P, "cfg1")
+    exp = G.expected(z, 0)
+    s = _lib.DeviceSearcher(0)
+    params = P.SearchParams(k=100, k_parallel=8, hops=3, mode="tc")
+    monkeypatch.setenv("GMPGR_SCRATCH_GB", "0.000001")
+    with pytest.raises(MemoryError):
+        P.c_hipanns_batch(idx, model, users[:32], emb, params, searcher=s)
+    monkeypatch.delenv("GMPGR_SCRATCH_GB")
+    with pytest.raises(P.InvalidArgumentError):
+        P.c_hipanns_batch(idx, model, users[:32, :10], emb, params, searcher=s)
+    r = P.c_hipanns_batch(idx, model, users[:32], emb, params, searcher=s)
+    np.testing.assert_array_equal(r.ids, exp["ids"][:32])
+    np.testing.assert_array_equal(r.scores, exp["scores"][:32])

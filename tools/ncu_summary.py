@@ -1,6 +1,10 @@
 """Summarise an ncu report (`--set full`) and a launch-list CSV into profiles/.
 
     python tools/ncu_summary.py <report.ncu-rep> <launches.csv> <n_queries> <out_prefix>
+                                [config k,kp,hops,ef mode]
+
+The optional trailer records what was captured (bench.py only uses a capture's traffic /
+tensor-pipe figures when config, params and mode match its own run).
 
 Writes <out_prefix>.json (key metrics per captured kernel + dram bytes per query) and
 <out_prefix>_sass_mix.txt (instruction mix / stall reasons of the top kernel).
@@ -71,7 +75,12 @@ def main():
             cnt[name] += 1
     tot = sum(per.values()) or 1.0
     share = {k: {"launches": cnt[k], "total_ns": v, "share": v / tot} for k, v in per.items()}
-    summary = {"report": rep, "n_queries": nq, "kernels": kernels,
+    extra = {}
+    if len(sys.argv) > 7:
+        k, kp, hops, ef = (int(v) for v in sys.argv[6].split(","))
+        extra = {"config": sys.argv[5], "params": {"k": k, "k_parallel": kp, "hops": hops, "ef": ef},
+                 "mode": sys.argv[7]}
+    summary = {"report": rep, "n_queries": nq, **extra, "kernels": kernels,
                "dram_bytes_per_launch": dram, "dram_bytes_per_query": dram / max(1, nq),
                "launch_list": share}
     json.dump(summary, open(prefix + ".json", "w"), indent=1)

@@ -30,7 +30,7 @@ def main():
     if os.environ.get("BAND"):
         kw["band_rel"] = kw["band_abs"] = float(os.environ["BAND"])
     torch.cuda.set_device(0)
-    wl = workload.make(cfg, n_queries=nq)
+    wl = workload.make(cfg, n_queries=nq, graph=os.environ.get("GMPGR_GRAPH", "gpu"))
     dm = wl.model.metric.device_model(0)
     g = wl.index.device_graph(0, items=wl.items)
     it = _lib.DeviceItems(wl.items, 0)
