@@ -207,6 +207,11 @@ struct gr_searcher {
         }
     } duo;
     int64_t duo_units_last = 0;  // resident units of the last duo launch (bench / tests)
+    // streamed host calls (gr_search with host buffers): copy-in / copy-out streams that run
+    // beside the kernel, chunk flags (avail, qdone[]) and their events
+    cudaStream_t s_in = nullptr, s_out = nullptr;
+    cudaEvent_t ev_reset = nullptr, ev_out = nullptr;
+    int *sflags = nullptr;  // [0] avail, [1 + c] queries finished in chunk c
     // staging for host-pointer calls
     DevBuf st_users, st_ids, st_scores, st_count, st_stats;
     size_t st_users_n = 0, st_out_n = 0, st_stats_n = 0;
@@ -1098,7 +1103,8 @@ int plan_duo(int k, int kp, SearchArgs &a) {
 // Duo kernel for the fixed model shapes; returns -1 if not applicable
 int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I, const float *users,
                int64_t Q, const gr_search_params *p, int64_t *ids, double *scores, int32_t *count,
-               int64_t *stats, cudaStream_t stream, int shape) {
+               int64_t *stats, cudaStream_t stream, int shape, const int *avail = nullptr,
+               int *qdone = nullptr, int chunk_q = 0) {
     SearchArgs a;
     std::memset(&a, 0, sizeof(a));
     const int mode = p->mode;
@@ -1215,10 +1221,103 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     a.queue = S->flags;
     a.nonfinite = S->flags + 1;
     a.band_viol = S->flags + 3;
+    a.avail = avail;
+    a.qdone = qdone;
+    a.chunk_q = chunk_q;
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
     kern<<<(int)(units / 2), 512, smem, stream>>>(a);
     GR_CUDA(cudaGetLastError());
     S->launches += 1;
+    return GR_OK;
+}
+
+// ------------------------------------------------------------------ streamed host calls
+// Stream memory operations (driver API, through the runtime's entry-point query).
+typedef CUresult (*StreamValueFn)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+struct MemOps {
+    StreamValueFn wait = nullptr, write = nullptr;
+    bool ok = false;
+};
+const MemOps &mem_ops() {
+    static MemOps m = [] {
+        MemOps r;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuStreamWaitValue32", &p, cudaEnableDefault, &q) == cudaSuccess && p &&
+            q == cudaDriverEntryPointSuccess)
+            r.wait = reinterpret_cast<StreamValueFn>(p);
+        p = nullptr;
+        if (cudaGetDriverEntryPoint("cuStreamWriteValue32", &p, cudaEnableDefault, &q) == cudaSuccess && p &&
+            q == cudaDriverEntryPointSuccess)
+            r.write = reinterpret_cast<StreamValueFn>(p);
+        cudaGetLastError();
+        r.ok = r.wait && r.write;
+        return r;
+    }();
+    return m;
+}
+
+// gr_search with host buffers, overlapped: users are copied in chunk by chunk on s_in while
+// the (single, persistent) duo kernel already runs -- each unit waits for its batch's chunk
+// (avail) -- and each chunk's results are copied out on s_out as soon as the kernel has
+// finished its queries (qdone[c], cuStreamWaitValue32).  So the e2e time is the kernel time
+// plus the first chunk's copy-in and the last chunk's copy-out.  Returns -1 when not
+// applicable (other kernels, small batches, no stream memory operations).
+int launch_streamed(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_items *I, const float *h_users,
+                    float *d_users, int64_t Q, const gr_search_params *p, int64_t *h_ids, double *h_scores,
+                    int32_t *h_count, int64_t *h_stats, int64_t *d_ids, double *d_scores, int32_t *d_count,
+                    int64_t *d_stats, int nst, cudaStream_t st) {
+    const char *kenv = getenv("GMPGR_KERNEL");
+    const char *senv = getenv("GMPGR_STREAM");
+    if ((kenv && *kenv) || (senv && senv[0] == '0') || Q < 4096) return -1;
+    const int shape = fixed_shape(M->dm);
+    if (!shape || (p->mode == GR_MODE_TC && !M->dm.tc_ok)) return -1;
+    const MemOps &mo = mem_ops();
+    if (!mo.ok) return -1;
+    constexpr int kChunks = 8;
+    if (!S->s_in) {
+        GR_CUDA(cudaStreamCreateWithFlags(&S->s_in, cudaStreamNonBlocking));
+        GR_CUDA(cudaStreamCreateWithFlags(&S->s_out, cudaStreamNonBlocking));
+        GR_CUDA(cudaEventCreateWithFlags(&S->ev_reset, cudaEventDisableTiming));
+        GR_CUDA(cudaEventCreateWithFlags(&S->ev_out, cudaEventDisableTiming));
+        if (int rc = dmalloc(&S->sflags, 1 + kChunks)) return rc;
+    }
+    const int d = M->dm.d_h, k = p->k;
+    const int chunk_q = (int)((((Q + kChunks - 1) / kChunks) + 7) / 8 * 8);
+    const int nchunks = (int)((Q + chunk_q - 1) / chunk_q);
+    GR_CUDA(cudaMemsetAsync(S->sflags, 0, (1 + kChunks) * sizeof(int), st));
+    GR_CUDA(cudaEventRecord(S->ev_reset, st));
+    // copy-in stream: chunk c's users, then avail = end of chunk c
+    GR_CUDA(cudaStreamWaitEvent(S->s_in, S->ev_reset, 0));
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t q0 = (int64_t)c * chunk_q, q1 = std::min<int64_t>(Q, q0 + chunk_q);
+        GR_CUDA(cudaMemcpyAsync(d_users + q0 * d, h_users + q0 * d, (size_t)(q1 - q0) * d * 4,
+                                cudaMemcpyHostToDevice, S->s_in));
+        if (mo.write((CUstream)S->s_in, (CUdeviceptr)S->sflags, (cuuint32_t)q1, 0) != CUDA_SUCCESS)
+            return fail(GR_ECUDA, "cuStreamWriteValue32 failed");
+    }
+    const int rc = launch_duo(S, G, M, I, d_users, Q, p, d_ids, d_scores, d_count, d_stats, st, shape,
+                              S->sflags, S->sflags + 1, chunk_q);
+    if (rc == -1) {  // the duo kernel does not take this call: drain the copy-in, plain path
+        GR_CUDA(cudaStreamSynchronize(S->s_in));
+        return -1;
+    }
+    if (rc) return rc;
+    // copy-out stream: each chunk as soon as its queries are finished
+    GR_CUDA(cudaStreamWaitEvent(S->s_out, S->ev_reset, 0));
+    for (int c = 0; c < nchunks; ++c) {
+        const int64_t q0 = (int64_t)c * chunk_q, q1 = std::min<int64_t>(Q, q0 + chunk_q), nq = q1 - q0;
+        if (mo.wait((CUstream)S->s_out, (CUdeviceptr)(S->sflags + 1 + c), (cuuint32_t)nq, 0 /*GEQ*/) != CUDA_SUCCESS)
+            return fail(GR_ECUDA, "cuStreamWaitValue32 failed");
+        GR_CUDA(cudaMemcpyAsync(h_ids + q0 * k, d_ids + q0 * k, (size_t)nq * k * 8, cudaMemcpyDeviceToHost, S->s_out));
+        GR_CUDA(cudaMemcpyAsync(h_scores + q0 * k, d_scores + q0 * k, (size_t)nq * k * 8, cudaMemcpyDeviceToHost,
+                                S->s_out));
+        GR_CUDA(cudaMemcpyAsync(h_count + q0, d_count + q0, (size_t)nq * 4, cudaMemcpyDeviceToHost, S->s_out));
+        GR_CUDA(cudaMemcpyAsync(h_stats + q0 * nst, d_stats + q0 * nst, (size_t)nq * nst * 8,
+                                cudaMemcpyDeviceToHost, S->s_out));
+    }
+    GR_CUDA(cudaEventRecord(S->ev_out, S->s_out));
+    GR_CUDA(cudaStreamWaitEvent(st, S->ev_out, 0));
     return GR_OK;
 }
 
@@ -1478,6 +1577,11 @@ int gr_searcher_destroy(gr_searcher *s) {
     }
     s->free_scratch();
     s->duo.free_all();
+    if (s->s_in) cudaStreamDestroy(s->s_in);
+    if (s->s_out) cudaStreamDestroy(s->s_out);
+    if (s->ev_reset) cudaEventDestroy(s->ev_reset);
+    if (s->ev_out) cudaEventDestroy(s->ev_out);
+    if (s->sflags) cudaFree(s->sflags);
     cudaFree(s->flags);
     cudaFree(s->counters);
     if (s->done) cudaEventDestroy(s->done);
@@ -1591,7 +1695,18 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
         if (int rc = stage<int64_t>(s->st_stats, cap_s, ns)) return rc;
         s->st_stats_n = cap_s;
         float *du = (float *)s->st_users.p;
-        if (attempt == 0) GR_CUDA(cudaMemcpyAsync(du, users, nu * 4, cudaMemcpyHostToDevice, st));
+        if (attempt == 0) {
+            if (m->dm.d_h != it->di.d) return fail(GR_EINVAL, "item embedding dim != model d_h");
+            if (g->max_row >= it->di.n) return fail(GR_EINVAL, "items table smaller than the graph");
+            const int rs = launch_streamed(s, g, m, it, users, du, Q, &pe, out_ids, out_scores, out_count,
+                                           out_stats, (int64_t *)s->st_ids.p, (double *)s->st_scores.p,
+                                           (int32_t *)s->st_count.p, (int64_t *)s->st_stats.p, nst, st);
+            if (rs != -1) {
+                if (rs) return rs;
+                goto launched;
+            }
+            GR_CUDA(cudaMemcpyAsync(du, users, nu * 4, cudaMemcpyHostToDevice, st));
+        }
         if (int rc = launch_search(s, g, m, it, du, Q, &pe, (int64_t *)s->st_ids.p,
                                    (double *)s->st_scores.p, (int32_t *)s->st_count.p,
                                    (int64_t *)s->st_stats.p, st))
@@ -1601,6 +1716,7 @@ int gr_search(gr_searcher *s, const gr_graph *g, const gr_model *m, const gr_ite
         GR_CUDA(cudaMemcpyAsync(out_count, s->st_count.p, (size_t)Q * 4, cudaMemcpyDeviceToHost, st));
         GR_CUDA(cudaMemcpyAsync(out_stats, s->st_stats.p, ns * 8, cudaMemcpyDeviceToHost, st));
     }
+launched:
     GR_CUDA(cudaEventRecord(s->done, st));
     int nonfinite = 0, band = 0;
     if (int rc = read_status(s, st, &nonfinite, &band)) return rc;

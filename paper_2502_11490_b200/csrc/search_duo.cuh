@@ -257,6 +257,18 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
         if (lt == 0) st.base = atomicAdd(a.queue, G);
         usync();
         if (st.base >= a.Q) break;
+        if (a.avail) {  // streamed call: wait until this batch's users have been copied in
+            if (lt == 0) {
+                const int need = (int)min((int64_t)st.base + G, a.Q);
+                int got;
+                for (;;) {
+                    asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(got) : "l"(a.avail) : "memory");
+                    if (got >= need) break;
+                    __nanosleep(500);
+                }
+            }
+            usync();
+        }
         if (lt < G) {
             MqQuery &Q = st.qs[lt];
             Q.q = st.base + lt < a.Q ? st.base + lt : -1;
@@ -569,17 +581,37 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     constexpr unsigned FULL = 0xffffffffu;
                     const int qend = st.qs[warp].f_off + st.qs[warp].f_cnt;
                     uint32_t *vb = vis_of(warp);
-                    auto meta = [&](int e0, int32_t &ms, int &len) {
-                        ms = -1;
-                        int32_t mgi = 0;
-                        const bool in = lane < RW && e0 + lane < qend;
-                        if (in) {
-                            GR_DCHECK(e0 + lane < capF, "fslot index %d >= %lld", e0 + lane, (long long)capF);
-                            ms = fslot[fc][e0 + lane];
-                            mgi = fsrch[fc][e0 + lane];
-                            GR_DCHECK(ms >= 0 && ms < g.n && (mgi >> 16) == warp, "frontier entry %d gi %x warp %d",
-                                      ms, mgi, warp);
+                    // the query's frontier entries stream through a two-window register buffer
+                    // (lane i holds entry wbase + i of the current window, and of the next):
+                    // batch boundaries come from shuffles, the list loads run a window ahead
+                    int wbase = st.qs[warp].f_off;
+                    int32_t cur_s = -1, cur_g = -1, nxt_s = -1, nxt_g = -1;
+                    auto load_win = [&](int base, int32_t &ws, int32_t &wg) {
+                        ws = -1;
+                        wg = -1;
+                        if (base + lane < qend) {
+                            GR_DCHECK(base + lane < capF, "fslot index %d >= %lld", base + lane, (long long)capF);
+                            ws = fslot[fc][base + lane];
+                            wg = fsrch[fc][base + lane];
+                            GR_DCHECK(ws >= 0 && ws < g.n && (wg >> 16) == warp, "frontier entry %d gi %x warp %d",
+                                      ws, wg, warp);
                         }
+                    };
+                    load_win(wbase, cur_s, cur_g);
+                    load_win(wbase + 32, nxt_s, nxt_g);
+                    auto meta = [&](int e0, int32_t &ms, int &len) {
+                        if (e0 >= wbase + 32) {  // advance the window (e0 < wbase + 64 always)
+                            wbase += 32;
+                            cur_s = nxt_s;
+                            cur_g = nxt_g;
+                            load_win(wbase + 32, nxt_s, nxt_g);
+                        }
+                        const int src = e0 - wbase + lane;  // < 64
+                        const int32_t a_s = __shfl_sync(FULL, cur_s, src & 31), a_g = __shfl_sync(FULL, cur_g, src & 31);
+                        const int32_t b_s = __shfl_sync(FULL, nxt_s, src & 31), b_g = __shfl_sync(FULL, nxt_g, src & 31);
+                        const bool in = lane < RW && e0 + lane < qend;
+                        ms = in ? (src < 32 ? a_s : b_s) : -1;
+                        const int32_t mgi = in ? (src < 32 ? a_g : b_g) : 0;
                         const int32_t head = __shfl_sync(FULL, mgi, 0);  // every lane: no short circuit
                         const bool same = in && mgi == head;
                         len = __popc(__ballot_sync(FULL, same));  // a prefix: entries sorted by searcher
@@ -792,6 +824,15 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 a.out_stats[q * nst + 2] = nr > 0 ? (pmeta(gq, c)[sv[0]] >> 1) : -1;
                 a.out_stats[q * nst + 3] = Q.rows;
                 a.out_stats[q * nst + 4] = Q.nbrs;
+            }
+        }
+        if (a.qdone) {  // streamed call: publish the finished queries of this batch
+            __threadfence();
+            usync();
+            if (lt == 0) {
+                int nq = 0;
+                for (int gq = 0; gq < G; ++gq) nq += st.qs[gq].q >= 0;
+                atomicAdd(a.qdone + st.base / a.chunk_q, nq);
             }
         }
         // ---- reset this unit's visited bitsets: zero the words of every claimed node (all

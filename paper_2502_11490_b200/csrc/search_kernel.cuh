@@ -80,6 +80,12 @@ struct SearchArgs {
     int64_t vis_words;
     int32_t *vlog;             // [units * G][log_cap]: claimed nodes of the running query
     int log_cap;
+    // streamed host calls (gr_search): users arrive in chunks while the kernel runs; a unit
+    // waits until *avail >= the end of its batch, and counts finished queries per chunk of
+    // chunk_q queries into qdone[] (the copy-out stream waits on those counters)
+    const int *avail;
+    int *qdone;
+    int chunk_q;
 };
 
 // Tensor-core mode certificate (run time).  The refinement argument (see below) needs
