@@ -278,3 +278,23 @@ def test_failed_call_leaves_the_searcher_usable(P, monkeypatch):
     r = P.c_hipanns_batch(idx, model, users[:32], emb, params, searcher=s)
     np.testing.assert_array_equal(r.ids, exp["ids"][:32])
     np.testing.assert_array_equal(r.scores, exp["scores"][:32])
+
+
+def test_streamed_host_call_equals_plain_path(P, monkeypatch):
+    """gr_search with host buffers and >= 4096 queries streams users in and results out in
+    chunks beside one persistent launch: identical results to the plain (copy, launch,
+    copy) path and to the reference's goldens for the first queries."""
+    from paper_2502_11490_b200 import workload
+
+    z, model, emb, _, idx = reference_workload(P, "cfg1")
+    _, _, users = workload.reference_inputs("cfg1", n_queries=6000)
+    exp = G.expected(z, 0)
+    params = P.SearchParams(k=100, k_parallel=8, hops=3, mode="tc")
+    a = P.c_hipanns_batch(idx, model, users, emb, params)
+    monkeypatch.setenv("GMPGR_STREAM", "0")
+    b = P.c_hipanns_batch(idx, model, users, emb, params)
+    for f in ("ids", "scores", "count", "evals", "per_layer", "hops_to_best", "rows_expanded", "nbr_ids_read"):
+        np.testing.assert_array_equal(getattr(a, f), getattr(b, f))
+    n = exp["ids"].shape[0]
+    np.testing.assert_array_equal(a.ids[:n], exp["ids"])
+    np.testing.assert_array_equal(a.scores[:n], exp["scores"])
