@@ -53,6 +53,7 @@ from .search import (
     c_hipanns_scores_batch,
     coverage,
     euclidean_scorer,
+    invalidate_device_items,
     model_scorer,
     recall_at,
     table_scorer,
@@ -69,4 +70,4 @@ __all__ = [
     "c_hipanns", "c_hipanns_batch", "c_hipanns_scores_batch", "coverage", "euclidean_scorer",
     "table_scorer", "create_model", "load_model", "model_scorer",
     "project", "quantize", "recall_at", "relevance", "relevance_batch", "save_model",
-]
+, "invalidate_device_items"]

@@ -89,7 +89,11 @@ _items_cache: dict = {}
 
 
 def device_items(emb, device: int | None = None) -> _lib.DeviceItems:
-    """Upload (once) an item-embedding array; cached while the array object lives."""
+    """Upload (once) an item-embedding array; cached while the array object lives.
+
+    The device copy is a SNAPSHOT taken at first use (the reference reads the live array on
+    every call, search.py:88): after editing an embedding array in place, call
+    ``invalidate_device_items(emb)`` (or pass a new array) so the next search re-uploads."""
     device = _lib.current_device() if device is None else device
     if isinstance(emb, np.ndarray):
         sig = (tuple(emb.shape), emb.dtype.str, emb.__array_interface__["data"][0])
@@ -102,6 +106,12 @@ def device_items(emb, device: int | None = None) -> _lib.DeviceItems:
     h = _lib.DeviceItems(emb, device)
     _items_cache[key] = (weakref.ref(emb, lambda _r, k=key: _items_cache.pop(k, None)), h, sig)
     return h
+
+
+def invalidate_device_items(emb) -> None:
+    """Drop every cached device copy of ``emb`` (after in-place edits)."""
+    for key in [k for k in _items_cache if k[0] == id(emb)]:
+        _items_cache.pop(key, None)
 
 
 class ModelScorer:
@@ -145,7 +155,8 @@ class EuclideanScorer:
         self._table = None
 
     def device_scores(self, device: int | None = None) -> _lib.DeviceScores:
-        if self._table is None:
+        device = _lib.current_device() if device is None else device
+        if self._table is None or self._table.device != device:
             self._table = _lib.DeviceScores(vectors=self.vectors, queries=self.query[None, :],
                                             device=device)
         return self._table
@@ -169,7 +180,8 @@ class TableScorer:
         self._table = None
 
     def device_scores(self, device: int | None = None) -> _lib.DeviceScores:
-        if self._table is None:
+        device = _lib.current_device() if device is None else device
+        if self._table is None or self._table.device != device:
             self._table = _lib.DeviceScores(self.scores[None, :], device=device)
         return self._table
 

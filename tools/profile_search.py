@@ -30,7 +30,9 @@ def main():
     if os.environ.get("BAND"):
         kw["band_rel"] = kw["band_abs"] = float(os.environ["BAND"])
     torch.cuda.set_device(0)
-    wl = workload.make(cfg, n_queries=nq, graph=os.environ.get("GMPGR_GRAPH", "gpu"))
+    wl = workload.make(cfg, n_queries=nq, graph=os.environ.get("GMPGR_GRAPH", "gpu"),
+                       n_items=int(os.environ["GMPGR_NITEMS"]) if os.environ.get("GMPGR_NITEMS") else None)
+    print(f"workload {cfg}: {wl.index._n} items, built in {wl.build_s:.1f}s", flush=True)
     dm = wl.model.metric.device_model(0)
     g = wl.index.device_graph(0, items=wl.items)
     it = _lib.DeviceItems(wl.items, 0)
@@ -60,6 +62,8 @@ def main():
               f"rows/q {stats[:,3].mean():.1f} nbrs/q {stats[:,4].mean():.1f}", flush=True)
     torch.cuda.profiler.stop()
     print("counters", s.counters(), flush=True)
+    free, total = torch.cuda.mem_get_info()
+    print(f"device memory: {(total - free) / 1e9:.1f} GB in use of {total / 1e9:.1f} GB", flush=True)
 
 
 if __name__ == "__main__":
