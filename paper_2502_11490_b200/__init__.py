@@ -70,4 +70,5 @@ __all__ = [
     "c_hipanns", "c_hipanns_batch", "c_hipanns_scores_batch", "coverage", "euclidean_scorer",
     "table_scorer", "create_model", "load_model", "model_scorer",
     "project", "quantize", "recall_at", "relevance", "relevance_batch", "save_model",
-, "invalidate_device_items"]
+    "invalidate_device_items",
+]
