@@ -312,7 +312,7 @@ def run_gmpgr(args):
 
     def measure(params: dict, steps: int, warmup: int, clocks: bool = False):
         """Device-timed search launches (CUDA events on the launching stream, max over ranks)."""
-        pc = SearchParams(**params, mode=args.mode)._c()
+        pc = SearchParams(**params, mode=args.mode, band_rel=args.band_rel, band_abs=args.band_abs)._c()
 
         def step():
             _lib.check(lib.gr_search_async(searcher.h, g.h, dm.h, it.h, users_d.data_ptr(), Q,
@@ -405,7 +405,7 @@ def run_gmpgr(args):
     h_sc = torch.empty((Q, k), dtype=torch.float64).pin_memory()
     h_cnt = torch.empty(Q, dtype=torch.int32).pin_memory()
     h_st = torch.empty((Q, 5 + L), dtype=torch.int64).pin_memory()
-    pc_main = SearchParams(**PARAMS, mode=args.mode)._c()
+    pc_main = SearchParams(**PARAMS, mode=args.mode, band_rel=args.band_rel, band_abs=args.band_abs)._c()
 
     def e2e_step():
         _lib.check(lib.gr_search(searcher.h, g.h, dm.h, it.h, pin_users.data_ptr(), Q,
@@ -597,6 +597,9 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--band-rel", type=float, default=0.0,
+                    help="tc-mode refinement band (relative part); <= 0: library default")
+    ap.add_argument("--band-abs", type=float, default=0.0)
     ap.add_argument("--graph", default="gpu", choices=["gpu", "exact"],
                     help="cfg3 graph: gpu = bulk GPU producer (builder.py, ~20 s); exact = the "
                          "reference's own construction algorithm (native exact parallel build, "
