@@ -128,6 +128,23 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     del centers, assign
     if graph == "exact":
         index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
+    elif graph == "random":  # memory/scale tests only: random fixed-degree layers, no quality
+        from .builder import draw_levels
+
+        levels = draw_levels(N, 1.0 / 17.0, 4, 0)
+        rng = np.random.default_rng(0)
+        layers = []
+        for l in range(int(levels.max()) + 1):
+            cap = 2 * m if l == 0 else m
+            members = np.nonzero(levels >= l)[0]
+            nb = np.zeros((N, cap), dtype=np.int32)
+            ct = np.zeros(N, dtype=np.int32)
+            if len(members) > 1:
+                nb[members] = members[rng.integers(0, len(members), size=(len(members), cap))]
+                ct[members] = cap
+            layers.append((nb, ct))
+        index = GraphIndex.from_arrays(np.arange(N, dtype=np.int64), levels, layers,
+                                       int(np.argmax(levels)), m=m, max_layers=4)
     else:
         index = GraphIndex.build(items, m=m, seed=0, device=dev, method="gpu")
     torch.cuda.synchronize(dev)

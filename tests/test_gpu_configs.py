@@ -281,15 +281,16 @@ def test_failed_call_leaves_the_searcher_usable(P, monkeypatch):
 
 
 def test_streamed_host_call_equals_plain_path(P, monkeypatch):
-    """gr_search with host buffers and >= 4096 queries streams users in and results out in
-    chunks beside one persistent launch: identical results to the plain (copy, launch,
-    copy) path and to the reference's goldens for the first queries."""
+    """gr_search with host buffers, >= 4096 queries and GMPGR_STREAM=1 streams users in and
+    results out in chunks beside one persistent launch: identical results to the plain
+    (copy, launch, copy) path and to the reference's goldens for the first queries."""
     from paper_2502_11490_b200 import workload
 
     z, model, emb, _, idx = reference_workload(P, "cfg1")
     _, _, users = workload.reference_inputs("cfg1", n_queries=6000)
     exp = G.expected(z, 0)
     params = P.SearchParams(k=100, k_parallel=8, hops=3, mode="tc")
+    monkeypatch.setenv("GMPGR_STREAM", "1")
     a = P.c_hipanns_batch(idx, model, users, emb, params)
     monkeypatch.setenv("GMPGR_STREAM", "0")
     b = P.c_hipanns_batch(idx, model, users, emb, params)
