@@ -20,6 +20,7 @@
 #include "search_kernel.cuh"
 #include "search_mq.cuh"
 #include "search_duo.cuh"
+#include "kernels.h"
 #include "scores.cuh"
 
 namespace {
@@ -934,13 +935,13 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
     case CODE:                                                                                     \
         if (g16) {                                                                                 \
             smem = plan_mq<DH, ZZ, 1, 512, 16, DH, true>(p->k, p->k_parallel, a);                  \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 16, DH, true>;                                \
+            kern = mq_kernel<DH, ZZ, 1, 512, 16, DH, true>();                                \
         } else if (pipe) {                                                                         \
             smem = plan_mq<DH, ZZ, 1, 512, 8, DH, true>(p->k, p->k_parallel, a);                   \
-            kern = hipanns_mq_kernel<DH, ZZ, 1, 512, 8, DH, true>;                                 \
+            kern = mq_kernel<DH, ZZ, 1, 512, 8, DH, true>();                                 \
         } else {                                                                                   \
             smem = plan_mq<DH, ZZ, 0, 512, 8, DH>(p->k, p->k_parallel, a);                         \
-            kern = hipanns_mq_kernel<DH, ZZ, 0, 512, 8, DH, false>;                                \
+            kern = mq_kernel<DH, ZZ, 0, 512, 8, DH, false>();                                \
         }                                                                                          \
         break;
     switch (shape) {
@@ -1116,10 +1117,10 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     case CODE:                                                               \
         if (mode == GR_MODE_TC) {                                            \
             smem = plan_duo<DH, ZZ, 1, GQ>(p->k, p->k_parallel, a);          \
-            kern = hipanns_duo_kernel<DH, ZZ, 1, GQ>;                        \
+            kern = duo_kernel<DH, ZZ, 1, GQ>();                        \
         } else {                                                             \
             smem = plan_duo<DH, ZZ, 0, GQ>(p->k, p->k_parallel, a);          \
-            kern = hipanns_duo_kernel<DH, ZZ, 0, GQ>;                        \
+            kern = duo_kernel<DH, ZZ, 0, GQ>();                        \
         }                                                                    \
         break;
     switch (shape) {
@@ -1405,20 +1406,20 @@ int launch_search(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr
     void (*kern)(const SearchArgs) = nullptr;
     if (mode == GR_MODE_TC) {
         switch (shape) {
-        case 1283: kern = hipanns_search_kernel<2, 128, 3, 1>; break;
-        case 1282: kern = hipanns_search_kernel<2, 128, 2, 1>; break;
-        case 643: kern = hipanns_search_kernel<2, 64, 3, 1>; break;
-        default: kern = hipanns_search_kernel<2, 64, 2, 1>; break;
+        case 1283: kern = search_kernel<2, 128, 3, 1>(); break;
+        case 1282: kern = search_kernel<2, 128, 2, 1>(); break;
+        case 643: kern = search_kernel<2, 64, 3, 1>(); break;
+        default: kern = search_kernel<2, 64, 2, 1>(); break;
         }
     } else {
         switch (shape) {
-        case 1283: kern = hipanns_search_kernel<2, 128, 3, 0>; break;
-        case 1282: kern = hipanns_search_kernel<2, 128, 2, 0>; break;
-        case 643: kern = hipanns_search_kernel<2, 64, 3, 0>; break;
-        case 642: kern = hipanns_search_kernel<2, 64, 2, 0>; break;
+        case 1283: kern = search_kernel<2, 128, 3, 0>(); break;
+        case 1282: kern = search_kernel<2, 128, 2, 0>(); break;
+        case 643: kern = search_kernel<2, 64, 3, 0>(); break;
+        case 642: kern = search_kernel<2, 64, 2, 0>(); break;
         default:
-            kern = smem <= 110 * 1024 ? hipanns_search_kernel<2, 0, 0, 0>
-                                      : hipanns_search_kernel<1, 0, 0, 0>;
+            kern = smem <= 110 * 1024 ? search_kernel<2, 0, 0, 0>()
+                                      : search_kernel<1, 0, 0, 0>();
         }
     }
     if (int rc = set_smem(kern, smem)) return rc;
@@ -1488,7 +1489,7 @@ int launch_search_scores(gr_searcher *S, const gr_graph *G, const gr_scores *T,
     a.off_sortv = P.alloc(a.sortcap * 4);
     a.off_kp = P.alloc(3 * p->k_parallel * 4);
     const int smem = P.bytes;
-    auto kern = smem <= 110 * 1024 ? hipanns_search_kernel<2, 0, 0, 2> : hipanns_search_kernel<1, 0, 0, 2>;
+    auto kern = smem <= 110 * 1024 ? search_kernel<2, 0, 0, 2>() : search_kernel<1, 0, 0, 2>();
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 0;
     GR_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, GR_NT, smem));

@@ -43,7 +43,7 @@ __device__ __forceinline__ uint64_t high_mask(int shift) {
 
 // Warp-cooperative: threshold of the top m among keys[0..n) (n > m >= 1).
 // hist: this warp's 256-entry shared histogram.
-__device__ uint64_t warp_select_threshold(const uint64_t *keys, int n, int m, uint32_t *hist) {
+static __device__ uint64_t warp_select_threshold(const uint64_t *keys, int n, int m, uint32_t *hist) {
     const int lane = threadIdx.x & 31;
     uint64_t prefix = 0;
     uint32_t rem = (uint32_t)m;
@@ -69,7 +69,7 @@ __device__ uint64_t warp_select_threshold(const uint64_t *keys, int n, int m, ui
 // CTA-cooperative version (all GR_NT threads call it).  hist: 256 shared u32;
 // bcast: 4 shared u32 scratch.
 template <int NT = GR_NT>
-__device__ uint64_t cta_select_threshold(const uint64_t *keys, int n, int m, uint32_t *hist,
+static __device__ uint64_t cta_select_threshold(const uint64_t *keys, int n, int m, uint32_t *hist,
                                          uint32_t *bcast) {
     const int tid = threadIdx.x;
     uint64_t prefix = 0;
@@ -101,7 +101,7 @@ __device__ uint64_t cta_select_threshold(const uint64_t *keys, int n, int m, uin
 // CTA bitonic sort, descending by key, of n entries (keys, vals) in shared memory
 // padded to cap (power of two >= n).  Padding keys are 0 (below every real key).
 template <int NT = GR_NT>
-__device__ void cta_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap) {
+static __device__ void cta_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap) {
     for (int i = n + threadIdx.x; i < cap; i += NT) { keys[i] = 0ull; vals[i] = -1; }
     __syncthreads();
     for (int size = 2; size <= cap; size <<= 1) {
@@ -125,7 +125,7 @@ __device__ void cta_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap) {
 // Bitonic sort (descending) by a group of GT threads synchronised with named barrier `bar`
 // (bar >= 1; barrier 0 is __syncthreads).  gtid: thread index inside the group.
 template <int GT>
-__device__ void group_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap, int gtid, int bar) {
+static __device__ void group_sort_desc(uint64_t *keys, int32_t *vals, int n, int cap, int gtid, int bar) {
     auto sync = [&]() {
         if constexpr (GT == 32) __syncwarp();
         else asm volatile("bar.sync %0, %1;" ::"r"(bar), "r"(GT) : "memory");

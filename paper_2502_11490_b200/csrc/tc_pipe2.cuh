@@ -9,11 +9,14 @@
 //   warps 5-7  TMA loaders: per 64-wide K chunk of a 128-pair tile, 64 tile::gather4 ops
 //              (32 four-row groups x hi/lo halves, 128-byte swizzled rows) over 96 lanes
 // Buffers per unit: S = 2 stages of one K chunk of the A operand (hi + lo, 32 KB each) in
-// shared memory; TMEM window of 256 columns: D0 [0,128) (layer 0: [0,64) = hi.W_hi + lo.W_hi,
-// [64,128) = hi.W_lo), D1 [128,192) (layer 1), A1 [192,256) (relu(layer 0) as bf16 hi|lo pairs).
+// shared memory; TMEM window of 256 columns: D0 double-buffered [0,64) / [64,128) (layer 0:
+// hi.W_hi + hi.W_lo + lo.W_hi accumulated in one fp32 accumulator), D1 [128,192) (layer 1),
+// A1 [192,256) (relu(layer 0) as bf16 hi|lo pairs).  With two D0 buffers the issuer runs
+// layer 0 of tile t+1 while the epilogue still works on tile t, so a stage is released as
+// soon as its MMAs retire and the next gathers start one epilogue earlier.
 // Hand-offs (mbarriers): full[s] (TMA tx) -> issuer, empty[s] commit -> loaders,
-// d0full commit -> E, d0empty E -> issuer, a1full E -> issuer, d1full commit -> E.
-// The single epilogue group serialises D0 / A1 / D1 reuse by program order.
+// d0full[b] commit -> E, d0empty[b] E -> issuer, a1full E -> issuer, d1full commit -> E.
+// The single epilogue group serialises A1 / D1 reuse by program order.
 #pragma once
 #include <cuda_bf16.h>
 
@@ -36,11 +39,10 @@ struct TcPipe2 {
     static constexpr int OFF_A = 0;                             // S chunk stages (hi, lo)
     static constexpr int A_REGION = S * 2 * CH_BYTES;           // 64 KB, aliased outside run()
     static constexpr int OFF_BAR = OFF_A + A_REGION;
-    enum { FULL0 = 0, EMPTY0 = S, D0FULL = 2 * S, D0EMPTY, A1FULL, D1FULL, NBAR };
+    enum { FULL0 = 0, EMPTY0 = S, D0FULL = 2 * S, D0EMPTY = 2 * S + 2, A1FULL = 2 * S + 4, D1FULL, NBAR };
     static constexpr int UNIT_BYTES = ((OFF_BAR + NBAR * 8 + 1023) / 1024) * 1024;
     static constexpr uint32_t IDESC = tc::idesc(TM, H);
-    static constexpr uint32_t IDESC_N128 = tc::idesc(TM, 2 * H);
-    static constexpr uint32_t C_D0 = 0, C_D1 = 128, C_A1 = 192, COLS = 256;
+    static constexpr uint32_t C_D0 = 0, C_D1 = 128, C_A1 = 192, COLS = 256;  // D0 buffer b at 64 b
 
     static __device__ __forceinline__ uint64_t *bar(unsigned char *u, int i) {
         return reinterpret_cast<uint64_t *>(u + OFF_BAR) + i;
@@ -53,8 +55,10 @@ struct TcPipe2 {
                 tc::mbar_init(bar(u, FULL0 + s), NOPS);
                 tc::mbar_init(bar(u, EMPTY0 + s), 1);
             }
-            tc::mbar_init(bar(u, D0FULL), 1);
-            tc::mbar_init(bar(u, D0EMPTY), NE);
+            for (int b = 0; b < 2; ++b) {
+                tc::mbar_init(bar(u, D0FULL + b), 1);
+                tc::mbar_init(bar(u, D0EMPTY + b), NE);
+            }
             tc::mbar_init(bar(u, A1FULL), NE);
             tc::mbar_init(bar(u, D1FULL), 1);
         }
@@ -113,7 +117,7 @@ struct TcPipe2 {
             }
         } else if (warp == ISSUER_WARP) {
             constexpr unsigned FULLM = 0xffffffffu;
-            const uint32_t bH0 = tc::smem_u32(sm + OFF_B0H);
+            const uint32_t bH0 = tc::smem_u32(sm + OFF_B0H), bL0 = tc::smem_u32(sm + OFF_B0L);
             const uint32_t bH1 = tc::smem_u32(sm + OFF_B1H), bL1 = tc::smem_u32(sm + OFF_B1L);
             auto ready = [&](int b, uint32_t par) {
                 return __shfl_sync(FULLM, lane == 0 ? (int)tc::mbar_test(bar(u, b), par) : 0, 0) != 0;
@@ -138,25 +142,26 @@ struct TcPipe2 {
                     }
                 }
                 if (l0t < T) {
-                    const uint32_t tg = tile_ctr + l0t;
+                    const uint32_t tg = tile_ctr + l0t, b = tg & 1u, use = tg >> 1;
                     const uint32_t qg = chunk_ctr + l0t * NC + l0k, s = qg % S, r = qg / S;
-                    // D0 of the previous tile must have been read by the epilogue
-                    if ((l0k != 0 || tg == 0 || ready(D0EMPTY, (tg - 1) & 1u)) && ready(FULL0 + s, r & 1u)) {
+                    // D0 buffer b must have been read by the epilogue (two tiles back)
+                    if ((l0k != 0 || use == 0 || ready(D0EMPTY + b, (use - 1) & 1u)) && ready(FULL0 + s, r & 1u)) {
                         tc::fence_async_smem();
                         tc::fence_after();
-                        const uint32_t d0 = tmem + C_D0;
+                        const uint32_t d0 = tmem + C_D0 + 64 * b;
                         const uint32_t aH = tc::smem_u32(u + OFF_A + s * 2 * CH_BYTES), aL = aH + CH_BYTES;
 #pragma unroll
                         for (int k = 0; k < KC / 16; ++k) {
                             const uint64_t ah = tc::desc_sw128(aH + k * 32), al = tc::desc_sw128(aL + k * 32);
                             const uint32_t kb = (l0k * (KC / 16) + k) * 256;
-                            const uint64_t bh = tc::desc(bH0 + kb, D_H);
-                            tc::mma_w(d0, ah, bh, IDESC_N128, (l0k | k) ? 1u : 0u);  // hi . [W_hi; W_lo]
-                            tc::mma_w(d0, al, bh, IDESC, 1u);                          // lo . W_hi
+                            const uint64_t bh = tc::desc(bH0 + kb, D_H), bl = tc::desc(bL0 + kb, D_H);
+                            tc::mma_w(d0, ah, bh, IDESC, (l0k | k) ? 1u : 0u);  // hi . W_hi
+                            tc::mma_w(d0, ah, bl, IDESC, 1u);                    // hi . W_lo
+                            tc::mma_w(d0, al, bh, IDESC, 1u);                    // lo . W_hi
                         }
                         tc::commit_w(bar(u, EMPTY0 + s));
                         if (++l0k == NC) {
-                            tc::commit_w(bar(u, D0FULL));
+                            tc::commit_w(bar(u, D0FULL + b));
                             l0k = 0;
                             ++l0t;
                         }
@@ -174,22 +179,20 @@ struct TcPipe2 {
                 const int gi = row < nv ? gis[base + row] : 0, gq = gi >> 16;
                 const int32_t my_s = row < nv ? slots[base + row] : 0;
                 const float *uq = U + gq * H;
-                tc::mbar_wait(bar(u, D0FULL), tg & 1u);
+                const uint32_t b = tg & 1u;
+                tc::mbar_wait(bar(u, D0FULL + b), (tg >> 1) & 1u);
                 tc::fence_after();
                 float h[64];
                 {
-                    const uint32_t d0 = tmem + lanebase + C_D0;
+                    const uint32_t d0 = tmem + lanebase + C_D0 + 64 * b;
+                    float va[32], vb[32];
+                    tc::tmem_ld32(d0, va);
+                    tc::tmem_ld32(d0 + 32, vb);
 #pragma unroll
-                    for (int half = 0; half < 2; ++half) {
-                        float va[32], vb[32];
-                        tc::tmem_ld32(d0 + 32 * half, va);
-                        tc::tmem_ld32(d0 + 64 + 32 * half, vb);
-#pragma unroll
-                        for (int j = 0; j < 32; ++j) h[32 * half + j] = va[j] + vb[j];
-                    }
+                    for (int j = 0; j < 32; ++j) { h[j] = va[j]; h[32 + j] = vb[j]; }
                 }
                 tc::fence_before();
-                tc::mbar_arrive(bar(u, D0EMPTY));
+                tc::mbar_arrive(bar(u, D0EMPTY + b));
                 const uint32_t a1 = tmem + lanebase + C_A1;
 #pragma unroll
                 for (int o = 0; o < 64; o += 16) {
