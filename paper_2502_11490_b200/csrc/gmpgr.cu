@@ -1139,7 +1139,7 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     const int64_t capP = p->k + capS;
     if (capS * GQ >= (1 << 24) || capP >= (1 << 24)) return -1;
     const int64_t hcap = 0;  // (query, node) hash: not needed (the first toucher is the owner)
-    const int64_t vwords = (G->dg.n + 15) / 16;
+    const int64_t vwords = (G->dg.n + 31) / 32;  // one visited bit per node
     const int64_t logcap = std::min<int64_t>(G->dg.n + 1, 1 << 16);
     if (int rc = set_smem(kern, smem)) return rc;
     int per_sm = 0;
@@ -1225,6 +1225,7 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     a.avail = avail;
     a.qdone = qdone;
     a.chunk_q = chunk_q;
+    if (const char *e = getenv("GMPGR_EXP")) a.exp = atoi(e);
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
     kern<<<(int)(units / 2), 512, smem, stream>>>(a);
     GR_CUDA(cudaGetLastError());

@@ -7,17 +7,20 @@
 // tiles are on the TMA / tcgen05 / epilogue warps -- the overlap a single lock-step CTA
 // cannot have (round-1 profile: expand 31% and score 40% of the launch, never concurrent).
 //
-// Visited state (claims) -- bounded by N/4 bytes per resident query, not 4N:
-//   two bits per node per query slot: D = claimed before this hop, T = touched this hop.
+// Visited state (claims) -- bounded by N/8 bytes per resident query, not 4N:
+//   one bit per node per query slot: set by the node's first touch (every first touch is a
+//   fresh claim, so "touched earlier this hop" and "claimed in an earlier hop" never need
+//   to be told apart).
 //   expand:  warp w of a unit owns query w and walks that query's frontier in list order
 //            (searcher-ascending, search.py:261-265) in batches that never span two searchers;
 //            a batch's claim atomics have all returned before the next batch issues its own.
-//            old = atomicOr(word, T):  D set -> already claimed;  T set -> touched earlier
-//            this hop by the same or a LOWER searcher;  neither -> first touch.  So the first
+//            old = atomicOr(word, bit): set -> claimed in an earlier hop, or touched earlier
+//            this hop by the same or a LOWER searcher; clear -> first touch.  So the first
 //            toucher is the lowest searcher listing the node -- the reference's lock-step
 //            ownership (search.py:220-224) -- with no second resolution pass.
-//   claim:   every first touch is fresh; D is set and the node is logged; at query end the
-//            logged nodes' words are zeroed (or the slot's whole bitset when the log overflowed).
+//   claim:   every first touch is fresh; the owning warp appends it to the survivors and to
+//            its query's claim log; at query end the logged nodes' words are zeroed (or the
+//            slot's whole bitset when the log overflowed).
 // MODE 0: exact-fp32 scoring of every claim (32-pair tiles per unit, weights in shared memory).
 // MODE 1: tcgen05 split-bf16 scoring of 128-pair tiles (tc_pipe2.cuh) + exact re-scoring of
 //         the band around every selection threshold, with the run-time band certificate.
@@ -300,8 +303,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
         // ================= helpers
         auto score_fresh = [&](int n, int layer, int hop) {
             auto on_score = [&](int i, bool valid, float v, int gi, int32_t s) {
-                const int gq = gi >> 16;
-                warp_count(&st.qs[gq].per_layer[layer], gq, 1, valid);
+                const int gq = gi >> 16;  // evaluations are counted per query by expand
                 if (valid && !isfinite(v)) atomicOr(a.nonfinite, 1);
                 const uint64_t key = make_key(v, slot_rank(g, s));
                 if (valid) fr_key[i] = key;
@@ -322,7 +324,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             };
             if constexpr (MODE == 1) {
                 TP::run(smem, ub, U, sb1, sW2, sb2, satt, tmem, a.it, g, fr_v, fr_i, n, chunk_ctr, tile_ctr, lt,
-                        on_score, usync, &a.hl_map);
+                        on_score, usync, &a.hl_map,
+                        a.phase_cycles && unit == 0 ? ph_acc + 8 : nullptr, a.exp);
                 if (lt == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
             } else {
                 int *pq = reinterpret_cast<int *>(sBuf + EX::OFF_PQ);
@@ -459,24 +462,20 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             }
             usync();
         };
-        // claim this hop's first touches [0, nS) (= the fresh claims): D bit + visited log
+        // this hop's first touches [0, nS) are the fresh claims (already in the visited bits and
+        // in their query's claim log, written by the owning warp during expand)
         auto resolve = [&](int nS) {
-            for (int t0 = 0; t0 < nS; t0 += NTH) {
-                const int t = t0 + lt;
-                const bool ok = t < nS;
-                int32_t v = 0, gq = 0;
-                if (ok) {
-                    v = surv_v[t];
-                    gq = surv_i[t] >> 16;
-                    GR_DCHECK(gq >= 0 && gq < G && v >= 0 && v < g.n, "resolve t %d gq %d v %d", t, gq, v);
-                    atomicOr(vis_of(gq) + (v >> 4), 1u << (2 * (v & 15)));
-                }
-                const int li = warp_append(gq, ok, [&](int q) { return &nlog[q]; });
-                if (ok && li < a.log_cap) log_of(gq)[li] = v;
-            }
-            usync();
             if (lt == 0) st.nFresh = nS;
             usync();
+        };
+        // append v (when ok) to query w's claim log; called by warp w (the only writer of nlog[w])
+        auto log_push = [&](int w, bool ok, int32_t v) {
+            const unsigned m = __ballot_sync(0xffffffffu, ok);
+            const int p = nlog[w] + __popc(m & ((1u << lane) - 1u));
+            if (ok && p < a.log_cap) log_of(w)[p] = v;
+            __syncwarp();
+            if (lane == 0) nlog[w] += __popc(m);
+            __syncwarp();
         };
         auto sort_pools = [&]() {
             const int gq = lt / GT, gt = lt % GT;
@@ -495,9 +494,11 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
         usync();
         if (lt < G && st.qs[lt].q >= 0) {
             const int idx = atomicAdd(&st.nS, 1);
-            atomicOr(vis_of(lt) + (g.entry >> 4), 2u << (2 * (g.entry & 15)));
+            atomicOr(vis_of(lt) + (g.entry >> 5), 1u << (g.entry & 31));
             surv_v[idx] = g.entry;
             surv_i[idx] = lt << 16;
+            log_of(lt)[0] = g.entry;
+            nlog[lt] = 1;
         }
         usync();
         if (warp < G && st.qs[warp].q >= 0) {
@@ -510,10 +511,12 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     const unsigned nv = __popc(__ballot_sync(0xffffffffu, v >= 0));
                     if (lane == 0) st.qs[warp].nbrs += nv;
                     uint32_t s2 = 1u;
-                    if (v >= 0) s2 = (atomicOr(vb + (v >> 4), 2u << (2 * (v & 15))) >> (2 * (v & 15))) & 3u;
+                    if (v >= 0) s2 = (atomicOr(vb + (v >> 5), 1u << (v & 31)) >> (v & 31)) & 1u;
                     warp_append2(v >= 0 && s2 == 0u, v, warp << 16, &st.nS, surv_v, surv_i);
+                    log_push(warp, v >= 0 && s2 == 0u, v);
                 }
             }
+            if (lane == 0) st.qs[warp].per_layer[top] = nlog[warp];  // entry + fresh neighbours
         }
         usync();
         resolve(st.nS);
@@ -593,6 +596,11 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             GR_DCHECK(base + lane < capF, "fslot index %d >= %lld", base + lane, (long long)capF);
                             ws = fslot[fc][base + lane];
                             wg = fsrch[fc][base + lane];
+                            if (layer == 0) {  // rows of the next batches: L2 ahead of the piece loads
+                                const char *rp = reinterpret_cast<const char *>(g.adj[0] + (int64_t)ws * g.ld[0]);
+                                for (int o = 0; o < g.ld[0] * 4; o += 128)
+                                    asm volatile("prefetch.global.L2 [%0];" ::"l"(rp + o));
+                            }
                             GR_DCHECK(ws >= 0 && ws < g.n && (wg >> 16) == warp, "frontier entry %d gi %x warp %d",
                                       ws, wg, warp);
                         }
@@ -632,6 +640,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     int len;
                     int4 pv[3];
                     int e0 = st.qs[warp].f_off;
+                    int lbase = nlog[warp];  // this query's claim log (warp-private during expand)
+                    int32_t *const lg = log_of(warp);
                     int32_t gi = meta(e0, ms, len);
                     pieces(ms, pv);
                     int nrows = 0, nnbr = 0;
@@ -639,13 +649,13 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         int32_t ms1;
                         int len1;
                         const int32_t gi1 = meta(e0 + len, ms1, len1);
-                        uint32_t s2[3][4];  // 2-bit states before this touch (bit0 D, bit1 T)
+                        uint32_t s2[3][4];  // visited bit before this touch
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
-                                s2[j][u] = vv[u] >= 0 ? atomicOr(vb + (vv[u] >> 4), 2u << (2 * (vv[u] & 15))) : 1u;
+                                s2[j][u] = vv[u] >= 0 ? atomicOr(vb + (vv[u] >> 5), 1u << (vv[u] & 31)) : 1u;
                         }
                         int4 pv1[3];
                         pieces(ms1, pv1);
@@ -655,7 +665,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u) {
-                                if (vv[u] >= 0) s2[j][u] = (s2[j][u] >> (2 * (vv[u] & 15))) & 3u;
+                                if (vv[u] >= 0) s2[j][u] = (s2[j][u] >> (vv[u] & 31)) & 1u;
                                 nv += vv[u] >= 0;
                                 cs += s2[j][u] == 0u;
                             }
@@ -669,6 +679,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         int bs = 0;
                         if (lane == 31 && is) bs = atomicAdd(&st.nS, is);
                         bs = __shfl_sync(FULL, bs, 31) + is - cs;
+                        int lp = lbase + is - cs;
+                        lbase += __shfl_sync(FULL, is, 31);
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
@@ -679,6 +691,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                                     surv_v[bs] = vv[u];
                                     surv_i[bs] = gi;
                                     ++bs;
+                                    if (lp < a.log_cap) lg[lp] = vv[u];
+                                    ++lp;
                                 }
                         }
                         nrows += len;
@@ -692,7 +706,12 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     }
 #pragma unroll
                     for (int o = 16; o > 0; o >>= 1) nnbr += __shfl_xor_sync(FULL, nnbr, o);
-                    if (lane == 0) { st.qs[warp].rows += nrows; st.qs[warp].nbrs += nnbr; }
+                    if (lane == 0) {
+                        st.qs[warp].rows += nrows;
+                        st.qs[warp].nbrs += nnbr;
+                        st.qs[warp].per_layer[layer] += lbase - nlog[warp];  // this hop's evaluations
+                        nlog[warp] = lbase;
+                    }
                 }
                 usync();
                 GR_PH(2);
@@ -842,7 +861,14 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             uint32_t *vb = vis_of(gq);
             if (nl <= a.log_cap) {
                 const int32_t *lg = log_of(gq);
-                for (int j = lt; j < nl; j += NTH) vb[lg[j] >> 4] = 0u;
+                for (int j0 = 0; j0 < nl; j0 += 4 * NTH) {
+                    int32_t v[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) v[u] = j0 + u * NTH + lt < nl ? lg[j0 + u * NTH + lt] : -1;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (v[u] >= 0) vb[v[u] >> 5] = 0u;
+                }
             } else {
                 for (int64_t w = lt; w < a.vis_words; w += NTH) vb[w] = 0u;
             }

@@ -76,7 +76,7 @@ struct SearchArgs {
     int32_t *cont_v, *cont_i;  // [units][capS] contested touches
     uint64_t *hash;            // [units][hash_cap] (query, node) -> survivor index
     int64_t hash_cap;
-    uint32_t *vis;             // [units * G][vis_words]: 2 bits per node (D, T)
+    uint32_t *vis;             // [units * G][vis_words]: 1 visited bit per node
     int64_t vis_words;
     int32_t *vlog;             // [units * G][log_cap]: claimed nodes of the running query
     int log_cap;
@@ -86,6 +86,7 @@ struct SearchArgs {
     const int *avail;
     int *qdone;
     int chunk_q;
+    int exp;  // GMPGR_EXP: timing experiments only (results not exact when set)
 };
 
 // Tensor-core mode certificate (run time).  The refinement argument (see below) needs

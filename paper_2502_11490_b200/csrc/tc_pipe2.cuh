@@ -76,8 +76,14 @@ struct TcPipe2 {
                                                const float *att, uint32_t tmem, const DevItems &it,
                                                const DevGraph &g, const int32_t *slots, const int32_t *gis,
                                                int n, uint32_t &chunk_ctr, uint32_t &tile_ctr, int lt,
-                                               OnScore on_score, Sync sync, const void *tmap) {
+                                               OnScore on_score, Sync sync, const void *tmap,
+                                               unsigned long long *tmr = nullptr, int exp = 0) {
+        // tmr (GMPGR_PHASE_TIMING, unit 0): [0] epilogue layer-0 work, [1] layer-1 work,
+        // [2] D0FULL wait, [3] D1FULL wait, [4] epilogue total, [5] issuer idle polls,
+        // [6] issuer issuing, [7] loader EMPTY wait (cycles of one thread per role)
         const int warp = lt >> 5, lane = lt & 31;
+        const bool timed = tmr && lane == 0;
+        auto clk = [&]() { return timed ? clock64() : 0ll; };
         const int T = (n + TM - 1) / TM;
         if (T == 0) return;
         // the A stages alias generic-proxy buffers outside run(): order those accesses before
@@ -107,7 +113,15 @@ struct TcPipe2 {
 #pragma unroll
                     for (int kc = 0; kc < NC; ++kc) {
                         const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, r = qg / S;
-                        if (r >= 1) tc::mbar_wait(bar(u, EMPTY0 + s), (r - 1) & 1u);
+                        if (r >= 1) {
+                            const long long c0 = clk();
+                            tc::mbar_wait(bar(u, EMPTY0 + s), (r - 1) & 1u);
+                            if (timed && lw == 0) tmr[7] += clk() - c0;
+                        }
+                        if ((exp & 1) && half) {  // experiment: hi rows only
+                            tc::mbar_arrive(bar(u, FULL0 + s));
+                            continue;
+                        }
                         tc::mbar_arrive_expect_tx(bar(u, FULL0 + s), 512);
                         tc::tma_gather4(tc::smem_u32(u + OFF_A + s * 2 * CH_BYTES) + half * CH_BYTES + grp * 512,
                                         tmap, half * D_H + kc * KC, cur[0], cur[1], cur[2], cur[3],
@@ -123,6 +137,10 @@ struct TcPipe2 {
                 return __shfl_sync(FULLM, lane == 0 ? (int)tc::mbar_test(bar(u, b), par) : 0, 0) != 0;
             };
             int l0t = 0, l0k = 0, l1t = 0;
+            long long c_last = clk();
+            auto acct = [&](int slot) {
+                if (timed) { const long long c = clock64(); tmr[slot] += c - c_last; c_last = c; }
+            };
             while (l1t < T) {
                 if (l1t < l0t) {  // layer 1 of an earlier tile as soon as its A1 is in TMEM
                     const uint32_t tg = tile_ctr + l1t;
@@ -138,6 +156,7 @@ struct TcPipe2 {
                         }
                         tc::commit_w(bar(u, D1FULL));
                         ++l1t;
+                        acct(6);
                         continue;
                     }
                 }
@@ -156,8 +175,10 @@ struct TcPipe2 {
                             const uint32_t kb = (l0k * (KC / 16) + k) * 256;
                             const uint64_t bh = tc::desc(bH0 + kb, D_H), bl = tc::desc(bL0 + kb, D_H);
                             tc::mma_w(d0, ah, bh, IDESC, (l0k | k) ? 1u : 0u);  // hi . W_hi
-                            tc::mma_w(d0, ah, bl, IDESC, 1u);                    // hi . W_lo
-                            tc::mma_w(d0, al, bh, IDESC, 1u);                    // lo . W_hi
+                            if (!(exp & 2)) {  // experiment 2: hi . W_hi only
+                                tc::mma_w(d0, ah, bl, IDESC, 1u);                // hi . W_lo
+                                tc::mma_w(d0, al, bh, IDESC, 1u);                // lo . W_hi
+                            }
                         }
                         tc::commit_w(bar(u, EMPTY0 + s));
                         if (++l0k == NC) {
@@ -165,14 +186,19 @@ struct TcPipe2 {
                             l0k = 0;
                             ++l0t;
                         }
+                        acct(6);
+                        continue;
                     }
                 }
+                acct(5);
             }
             __syncwarp();
         } else {
             // ================= epilogue: row = TMEM lane
             const int q4 = warp & 3, row = q4 * 32 + lane;
             const uint32_t lanebase = (uint32_t)(q4 * 32) << 16;
+            const bool et = timed && warp == 0;
+            const long long e_start = et ? clock64() : 0;
             for (int t = 0; t < T; ++t) {
                 const uint32_t tg = tile_ctr + t;
                 const int base = t * TM, nv = min(TM, n - base);
@@ -180,16 +206,13 @@ struct TcPipe2 {
                 const int32_t my_s = row < nv ? slots[base + row] : 0;
                 const float *uq = U + gq * H;
                 const uint32_t b = tg & 1u;
+                long long c0 = et ? clock64() : 0;
                 tc::mbar_wait(bar(u, D0FULL + b), (tg >> 1) & 1u);
+                if (et) { const long long c = clock64(); tmr[2] += c - c0; c0 = c; }
                 tc::fence_after();
                 float h[64];
                 {
-                    const uint32_t d0 = tmem + lanebase + C_D0 + 64 * b;
-                    float va[32], vb[32];
-                    tc::tmem_ld32(d0, va);
-                    tc::tmem_ld32(d0 + 32, vb);
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) { h[j] = va[j]; h[32 + j] = vb[j]; }
+                    tc::tmem_ld64(tmem + lanebase + C_D0 + 64 * b, h);
                 }
                 tc::fence_before();
                 tc::mbar_arrive(bar(u, D0EMPTY + b));
@@ -213,14 +236,14 @@ struct TcPipe2 {
                 tc::tmem_wait_st();
                 tc::fence_before();
                 tc::mbar_arrive(bar(u, A1FULL));
+                if (et) { const long long c = clock64(); tmr[0] += c - c0; c0 = c; }
                 tc::mbar_wait(bar(u, D1FULL), tg & 1u);
+                if (et) { const long long c = clock64(); tmr[3] += c - c0; c0 = c; }
                 tc::fence_after();
                 {
-                    float va[32], vb[32];
-                    tc::tmem_ld32(tmem + lanebase + C_D1, va);
-                    tc::tmem_ld32(tmem + lanebase + C_D1 + 32, vb);
+                    tc::tmem_ld64(tmem + lanebase + C_D1, h);
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) { h[j] = fmaxf(va[j] + b1[j], 0.f); h[32 + j] = fmaxf(vb[j] + b1[32 + j], 0.f); }
+                    for (int j = 0; j < 64; ++j) h[j] = fmaxf(h[j] + b1[j], 0.f);
                 }
                 tc::fence_before();
                 // approximate path (reassociated): the exact refinement re-scores every item
@@ -249,7 +272,9 @@ struct TcPipe2 {
                     s = fmaf(z, att[o], s);
                 }
                 on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s, gi, my_s);
+                if (et) tmr[1] += clock64() - c0;
             }
+            if (et) tmr[4] += clock64() - e_start;
         }
         chunk_ctr += T * NC;
         tile_ctr += T;
