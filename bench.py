@@ -9,8 +9,13 @@ top-100, SearchParams(k=100, k_parallel=8, hops=3, ef=200) (reference defaults,
 evalharness.py:84-87), a 65,536-query batch per GPU (weak scaling: every rank holds a
 replica of the index and searches its own query batch; no data-path collective).
 
+Graph: the reference's own construction algorithm (GraphIndex.build(m=24,
+ef_construction=64, seed=0), native exact parallel build, cached on the box's local
+disk); the line's `own_graph` block repeats the search on this repo's bulk GPU graph
+producer over the same items (--graph gpu makes that the headline instead).
+
 A step = one batched C-HiPANNS over the per-GPU query batch = ONE launch of
-hipanns_search_kernel (exact-fp32 scoring fused).  `value` uses device-resident
+hipanns_duo_kernel (tcgen05 scoring + exact refinement fused).  `value` uses device-resident
 inputs, CUDA events on the launching stream, max over ranks.  `e2e` goes through the
 public host API (host buffers, H2D of users + D2H of ids/scores/stats inside the
 timed region).  `--impl reference` times the reference algorithm's CPU restatement
@@ -242,7 +247,7 @@ def config_of(args, wl):
                       else "GPU producer (builder.py): reference level draws + symmetric pruned k-NN")}
 
 
-def ncu_profile(kernel: str, per_launch_s: float, config: str, mode: str):
+def ncu_profile(kernel: str, per_launch_s: float, config: str, mode: str, graph: str = "gpu"):
     """The committed ncu --set full summary for THIS run's kernel, or None: the capture must
     name the same kernel instantiation, the same config/params/mode, and its launch duration
     must be within 25% of this run's CUDA-event launch time (ncu runs cold, serialised)."""
@@ -250,7 +255,8 @@ def ncu_profile(kernel: str, per_launch_s: float, config: str, mode: str):
         prof = json.load(open(os.path.join(ROOT, "profiles", "ncu_search_kernel.json")))
     except Exception:
         return None
-    if prof.get("config") != config or prof.get("params") != dict(PARAMS) or prof.get("mode") != mode:
+    if (prof.get("config") != config or prof.get("params") != dict(PARAMS) or prof.get("mode") != mode
+            or prof.get("graph", "gpu") != graph):
         return None
     for k in prof.get("kernels", []):
         if kernel not in k.get("kernel", ""):
@@ -310,12 +316,13 @@ def run_gmpgr(args):
     flush = (torch.empty(64 << 20, dtype=torch.float32, device=f"cuda:{dev}")
              if n_items * d_items * 4 <= 2 * 126e6 else None)
 
-    def measure(params: dict, steps: int, warmup: int, clocks: bool = False):
+    def measure(params: dict, steps: int, warmup: int, clocks: bool = False, graph=None):
         """Device-timed search launches (CUDA events on the launching stream, max over ranks)."""
         pc = SearchParams(**params, mode=args.mode, band_rel=args.band_rel, band_abs=args.band_abs)._c()
+        gh = (graph or g).h
 
         def step():
-            _lib.check(lib.gr_search_async(searcher.h, g.h, dm.h, it.h, users_d.data_ptr(), Q,
+            _lib.check(lib.gr_search_async(searcher.h, gh, dm.h, it.h, users_d.data_ptr(), Q,
                                            ctypes.byref(pc), out_ids.data_ptr(), out_sc.data_ptr(),
                                            out_cnt.data_ptr(), out_st.data_ptr(), sp))
 
@@ -375,7 +382,8 @@ def run_gmpgr(args):
     fp32_peak = 148 * 128 * sm_mhz * 1e6 / 1e12  # separate fmul/fadd issue, TFLOP/s
     kname = ("hipanns_mq_kernel" if os.environ.get("GMPGR_KERNEL") == "mq" else "hipanns_duo_kernel") \
         if d_h in (64, 128) else "hipanns_search_kernel"
-    prof = ncu_profile(kname, per_launch, args.config, args.mode)
+    prof = ncu_profile(kname, per_launch, args.config, args.mode,
+                       "reference" if args.config in ("cfg1", "cfg2") else args.graph)
     traffic = tensor_ncu = None
     if prof:
         kp_ = prof[1]
@@ -501,6 +509,31 @@ def run_gmpgr(args):
                                                       m["scores"][:nq], m["evals"][:nq])
             ops.append(op)
         line["operating_points"] = ops
+    line["resident_units"] = searcher.counters().get("resident_units")
+    # ---- the same queries on this repo's own bulk GPU graph producer (builder.py): a second
+    # graph of the same items (the exact-graph line above is the reference-faithful headline)
+    if args.graph == "exact" and args.own_graph and args.config not in ("cfg1", "cfg2"):
+        t0 = time.perf_counter()
+        from paper_2502_11490_b200.index import GraphIndex
+
+        gidx = GraphIndex.build(wl.items, m=index.m, seed=0, device=torch.device("cuda", dev), method="gpu")
+        torch.cuda.synchronize(dev)
+        torch.cuda.empty_cache()
+        g2 = gidx.device_graph(dev, items=wl.items)
+        build2 = time.perf_counter() - t0
+        own = {"graph": "GPU producer (builder.py): reference level draws + symmetric pruned k-NN",
+               "build_s": build2, "points": []}
+        for prm, steps in ((dict(PARAMS), 3), (dict(PARAMS, k_parallel=32, hops=10), 2)):
+            if not args.operating_points and prm != dict(PARAMS):
+                continue
+            m = measure(prm, steps, 1, graph=g2)
+            b = algorithmic_bytes(m["evals"], m["rows"], m["nbrs"], d_h, k)
+            own["points"].append({"params": prm, "value": Q * steps * world / m["elapsed"], "unit": "queries/s",
+                                  "ms_per_step": 1000 * m["elapsed"] / steps, "recall_at_100": recall_of(m["ids"]),
+                                  "mean_evals_per_query": float(m["evals"].mean()),
+                                  "roofline_frac": b / m["per_launch"] / 1e9 / pk["hbm_gbs"]})
+        line["own_graph"] = own
+        del g2, gidx
     if want_cpu and rank == 0:
         r, n, t, threads = cpu_baseline(wl, target_s=args.cpu_s)
         line["cpu_baseline"] = {"value": n / t, "unit": "queries/s", "cores": threads,
@@ -600,10 +633,13 @@ def main():
     ap.add_argument("--band-rel", type=float, default=0.0,
                     help="tc-mode refinement band (relative part); <= 0: library default")
     ap.add_argument("--band-abs", type=float, default=0.0)
-    ap.add_argument("--graph", default="gpu", choices=["gpu", "exact"],
-                    help="cfg3 graph: gpu = bulk GPU producer (builder.py, ~20 s); exact = the "
-                         "reference's own construction algorithm (native exact parallel build, "
-                         "minutes at 10M items)")
+    ap.add_argument("--graph", default="exact", choices=["gpu", "exact"],
+                    help="cfg3 graph: exact (default) = the reference's own construction algorithm "
+                         "(GraphIndex.build, native exact parallel build: ~3.5 min at 10M items on "
+                         "16 host cores, cached under GMPGR_CACHE for later runs on the box); gpu = "
+                         "the bulk GPU producer (builder.py, ~20 s)")
+    ap.add_argument("--no-own-graph", dest="own_graph", action="store_false",
+                    help="skip the extra record on the GPU-producer graph (exact-graph runs)")
     ap.add_argument("--no-operating-points", dest="operating_points", action="store_false",
                     help="skip the extra kp=32/hops=10 (high-recall) operating point")
     ap.add_argument("--k-parallel", type=int, default=PARAMS["k_parallel"],

@@ -161,11 +161,12 @@ int64_t gr_searcher_launches(const gr_searcher *s);
 /* cumulative scoring counters of this searcher: out[0] = exact re-scores (tensor-core
  * mode), out[1] = tensor-core scores; when the searcher was created with
  * GMPGR_PHASE_TIMING=1 in the environment, out[2..9] = summed SM cycles per search phase
- * (init, seeds, expand, resolve, score, pool, frontier, output) and out[10..14] = cycles
- * inside tensor-core tiles (gather, layer-0 MMA wait, epilogue 0, layer-1 MMA wait,
- * epilogue 1); out[18] = band violations seen (exact re-scores whose approximate score was
+ * (init, seeds, expand, resolve, score, pool, frontier, output) and out[10..17] = cycles
+ * of the duo kernel's tensor-core stage roles (epilogue layer-0 / layer-1 work, layer-0 /
+ * layer-1 waits, epilogue total, issuer idle / issuing, loader stage waits); out[18] = band violations seen (exact re-scores whose approximate score was
  * farther than band/2 from the exact one), out[19] = largest |approx - exact| / band seen,
- * as f32 bits, out[20] = batches gr_search re-ran in exact mode.  out must hold 22 values.
+ * as f32 bits, out[20] = batches gr_search re-ran in exact mode, out[21] = resident search
+ * units (CTA halves of 8 queries) of the last duo-kernel launch.  out must hold 22 values.
  * Synchronises the device. */
 int gr_searcher_counters(gr_searcher *s, int64_t *out);
 

@@ -285,7 +285,7 @@ class DeviceSearcher(_Handle):
         d = {"exact_rescored": int(out[0]), "tensor_scored": int(out[1]),
              "band_violations": int(out[18]),
              "max_err_over_band": float(np.array([out[19]], dtype=np.uint32).view(np.float32)[0]),
-             "exact_reruns": int(out[20])}
+             "exact_reruns": int(out[20]), "resident_units": int(out[21])}
         if out[2:10].any():
             names = ("init", "seeds", "expand", "resolve", "score", "pool", "frontier", "output")
             tot = float(out[2:10].sum())

@@ -1615,6 +1615,7 @@ int gr_searcher_counters(gr_searcher *s, int64_t *out) {
     out[18] = (int64_t)c[2];
     out[19] = (int64_t)c[3];
     out[20] = s->band_reruns;
+    out[21] = s->duo_units_last;
     return GR_OK;
 }
 

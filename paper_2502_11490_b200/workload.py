@@ -127,7 +127,7 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     torch.backends.cuda.matmul.allow_tf32 = prev
     del centers, assign
     if graph == "exact":
-        index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
+        index = exact_graph(name, items, m, rank)
     elif graph == "random":  # memory/scale tests only: random fixed-degree layers, no quality
         from .builder import draw_levels
 
@@ -152,6 +152,44 @@ def make(name: str, rank: int = 0, device: int = 0, host_items: bool = False,
     items_host = items.cpu().numpy() if host_items else None
     return Workload(name, model, items, items_host, np.ascontiguousarray(users, np.float32), index,
                     time.perf_counter() - t0)
+
+
+def exact_graph(name: str, items, m: int, rank: int = 0) -> GraphIndex:
+    """GraphIndex.build(items, m, ef_construction=64, seed=0) -- the reference's own
+    construction algorithm (native exact parallel build) -- cached on local disk
+    (GMPGR_CACHE, default /tmp/gmpgr_cache) keyed by the items' digest, so the ranks of one
+    box and the benchmark's two arms build it once: rank 0 builds, the others wait for the
+    file."""
+    import hashlib
+    import os
+
+    N, d = items.shape
+    probe = items[:: max(1, N // 8192)].double().cpu().numpy()
+    key = hashlib.sha256(probe.tobytes()).hexdigest()[:16]
+    cache = os.environ.get("GMPGR_CACHE", "/tmp/gmpgr_cache")
+    path = os.path.join(cache, f"{name}_{N}x{d}_m{m}_ef64_{key}.npz")
+    if not os.path.exists(path):
+        if rank == 0:
+            index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
+            ids, levels, layers, entry = index.graph_view()
+            os.makedirs(cache, exist_ok=True)
+            arrs = {"ids": ids, "levels": levels, "entry": np.int64(entry), "m": np.int64(index.m),
+                    "max_layers": np.int64(index.max_layers)}
+            for l, (nb, ct) in enumerate(layers):
+                arrs[f"nb{l}"], arrs[f"ct{l}"] = nb, ct
+            tmp = path + f".tmp{os.getpid()}.npz"
+            np.savez(tmp, **arrs)
+            os.replace(tmp, path)
+            return index
+        t0 = time.time()
+        while not os.path.exists(path):
+            if time.time() - t0 > 3600:
+                raise TimeoutError(f"rank {rank}: no graph from rank 0 at {path}")
+            time.sleep(2.0)
+    z = np.load(path)
+    nl = sum(1 for f in z.files if f.startswith("nb"))
+    return GraphIndex.from_arrays(z["ids"], z["levels"], [(z[f"nb{l}"], z[f"ct{l}"]) for l in range(nl)],
+                                  int(z["entry"]), m=int(z["m"]), max_layers=int(z["max_layers"]))
 
 
 def make_shard(rank: int, world: int, shard_n: int = 12_500_000, d: int = 128, m: int = 24,

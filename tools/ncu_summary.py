@@ -1,7 +1,7 @@
 """Summarise an ncu report (`--set full`) and a launch-list CSV into profiles/.
 
     python tools/ncu_summary.py <report.ncu-rep> <launches.csv> <n_queries> <out_prefix>
-                                [config k,kp,hops,ef mode]
+                                [config k,kp,hops,ef mode [graph]]
 
 The optional trailer records what was captured (bench.py only uses a capture's traffic /
 tensor-pipe figures when config, params and mode match its own run).
@@ -79,7 +79,7 @@ def main():
     if len(sys.argv) > 7:
         k, kp, hops, ef = (int(v) for v in sys.argv[6].split(","))
         extra = {"config": sys.argv[5], "params": {"k": k, "k_parallel": kp, "hops": hops, "ef": ef},
-                 "mode": sys.argv[7]}
+                 "mode": sys.argv[7], "graph": sys.argv[8] if len(sys.argv) > 8 else "gpu"}
     summary = {"report": rep, "n_queries": nq, **extra, "kernels": kernels,
                "dram_bytes_per_launch": dram, "dram_bytes_per_query": dram / max(1, nq),
                "launch_list": share}
