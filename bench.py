@@ -186,6 +186,72 @@ def cpu_baseline(wl, target_s=15.0):
     return r, n, t, threads
 
 
+REF_PKG = os.path.join(ROOT, "baseline", "_ref")  # pip-installed /root/reference (nann), if present
+_STOCK = {}
+
+
+def _stock_one(q):
+    from nann import SearchParams as RefParams, c_hipanns as ref_c_hipanns, model_scorer as ref_scorer
+
+    g = _STOCK
+    t0 = time.perf_counter()
+    r = ref_c_hipanns(g["index"], ref_scorer(g["model"], g["users"][q], g["items"]), RefParams(**g["params"]))
+    dt = time.perf_counter() - t0
+    ids = np.full(g["params"]["k"], -1, np.int64)
+    sc = np.full(g["params"]["k"], np.nan)
+    for j, (i, v) in enumerate(r.items):
+        ids[j], sc[j] = i, v
+    return q, ids, sc, int(r.stats.metric_evaluations), dt
+
+
+def stock_reference(wl, queries, params, processes=1, budget_s=None):
+    """The UNMODIFIED reference package (nann, pip-installed from /root/reference into
+    baseline/_ref) searching this workload: nann.GraphIndex.load of this index's NANN-IDX
+    file, nann.create_model(d, d, Z, (64, 64), seed=1) (the same weights), model_scorer over
+    the same item embeddings, nann.c_hipanns with the same SearchParams -- in `processes`
+    forked processes.  With budget_s, queries are taken in order until the budget is spent.
+    Returns (ids, scores, evals, n_done, seconds) or None when nann is not installed."""
+    if not os.path.isdir(os.path.join(REF_PKG, "nann")):
+        return None
+    import multiprocessing as mp
+
+    if REF_PKG not in sys.path:
+        sys.path.insert(0, REF_PKG)
+    from nann import GraphIndex as RefIndex, create_model as ref_create_model
+
+    cache = os.environ.get("GMPGR_CACHE", "/tmp/gmpgr_cache")
+    os.makedirs(cache, exist_ok=True)
+    from paper_2502_11490_b200 import workload as W
+
+    path = os.path.join(cache, f"{wl.name}_{W.graph_digest(wl.index)[:16]}.nannidx")
+    if not os.path.exists(path):
+        wl.index.save(path + ".tmp")
+        os.replace(path + ".tmp", path)
+    d = wl.model.d_h
+    _STOCK.update(index=RefIndex.load(path),
+                  model=ref_create_model(d_x=d, d_h=d, z_dim=wl.model.z_dim, hidden=(64, 64), seed=1),
+                  users=wl.users, items=wl.items_host, params=dict(params))
+    queries = list(queries)
+    out = []
+    t0 = time.perf_counter()
+    if processes <= 1:
+        for q in queries:
+            out.append(_stock_one(q))
+            if budget_s and time.perf_counter() - t0 > budget_s:
+                break
+    else:
+        with mp.get_context("fork").Pool(processes) as pool:
+            for r in pool.imap(_stock_one, queries, chunksize=1):
+                out.append(r)
+                if budget_s and time.perf_counter() - t0 > budget_s:
+                    pool.terminate()
+                    break
+    elapsed = time.perf_counter() - t0
+    out.sort(key=lambda r: r[0])
+    return (np.stack([r[1] for r in out]), np.stack([r[2] for r in out]),
+            np.array([r[3] for r in out]), len(out), elapsed)
+
+
 def run_reference(args):
     dist, rank, world, local = dist_setup(args.gpus)
     if rank != 0:
@@ -222,6 +288,17 @@ def run_reference(args):
                 "d2h_bytes_per_step": 0},
         "gpu_launches": 0,
     }
+    # the unmodified reference package itself (nann from baseline/_ref), all host cores as
+    # processes, on the first queries of the same batch -- and the oracle port's agreement
+    st = stock_reference(wl, range(len(wl.users)), PARAMS, processes=threads, budget_s=args.stock_s)
+    if st is not None:
+        ids_s, sc_s, ev_s, n_s, t_s = st
+        r_o, _ = cpu_search(wl, wl.users[:n_s], threads)
+        line["stock_reference"] = {
+            "value": n_s / t_s, "unit": "queries/s", "processes": threads,
+            "sample": f"first {n_s} queries of the batch, nann.c_hipanns + model_scorer (the unmodified "
+                      f"reference package, pip-installed into baseline/_ref), {threads} processes, {t_s:.1f}s",
+            "oracle_port_vs_stock": parity_vs(ids_s, sc_s, ev_s, r_o["ids"], r_o["scores"], r_o["evals"])}
     emit(line)
     if dist:
         dist.destroy_process_group()
@@ -544,6 +621,15 @@ def run_gmpgr(args):
         line["cpu_reference_check"] = parity_vs(r["ids"], r["scores"], r["evals"], dev_ids[:n],
                                                 dev_scores[:n], evals[:n])
         line["ids_identical_to_cpu_reference"] = line["cpu_reference_check"]["ids_identical"]
+        # the unmodified reference package (nann, baseline/_ref) on the first queries
+        nq = min(Q, args.stock_queries)
+        st = stock_reference(wl, range(nq), PARAMS, processes=1) if nq else None
+        if st is not None:
+            ids_s, sc_s, ev_s, n_s, t_s = st
+            line["stock_reference_check"] = dict(
+                parity_vs(ids_s, sc_s, ev_s, dev_ids[:n_s], dev_scores[:n_s], evals[:n_s]),
+                source="nann.c_hipanns + model_scorer, unmodified reference package (baseline/_ref)",
+                seconds_per_query_1_process=t_s / max(1, n_s))
     if rank == 0:
         emit(line)
     if dist:
@@ -630,6 +716,10 @@ def main():
     ap.add_argument("--cpu-s", type=float, default=15.0)
     ap.add_argument("--ref-step-s", type=float, default=8.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--stock-queries", type=int, default=16,
+                    help="queries checked against the unmodified reference package (baseline/_ref)")
+    ap.add_argument("--stock-s", type=float, default=20.0,
+                    help="--impl reference: seconds of the unmodified reference package's timing")
     ap.add_argument("--band-rel", type=float, default=0.0,
                     help="tc-mode refinement band (relative part); <= 0: library default")
     ap.add_argument("--band-abs", type=float, default=0.0)
