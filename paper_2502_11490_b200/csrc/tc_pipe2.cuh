@@ -115,7 +115,8 @@ struct TcPipe2 {
                         const uint32_t qg = chunk_ctr + t * NC + kc, s = qg % S, r = qg / S;
                         if (r >= 1) {
                             const long long c0 = clk();
-                            tc::mbar_wait(bar(u, EMPTY0 + s), (r - 1) & 1u);
+                            // suspended, not spinning: the epilogue warps share these SMSPs
+                            tc::mbar_wait_hint(bar(u, EMPTY0 + s), (r - 1) & 1u, 2000u);
                             if (timed && lw == 0) tmr[7] += clk() - c0;
                         }
                         if ((exp & 1) && half) {  // experiment: hi rows only
@@ -190,6 +191,7 @@ struct TcPipe2 {
                         continue;
                     }
                 }
+                __nanosleep(100);  // nothing ready: yield the SMSP to the epilogue warps
                 acct(5);
             }
             __syncwarp();

@@ -68,6 +68,19 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase) {
             : "memory");
     }
 }
+// wait with a suspend-time hint (ns): the warp may be descheduled until the phase completes
+// (or the hint elapses) instead of re-issuing the probe
+__device__ __forceinline__ void mbar_wait_hint(uint64_t *bar, uint32_t phase, uint32_t ns) {
+    uint32_t ok = 0;
+    while (!ok) {
+        asm volatile(
+            "{\n\t.reg .pred P1;\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+            "selp.b32 %0, 1, 0, P1;\n\t}"
+            : "=r"(ok)
+            : "r"(smem_u32(bar)), "r"(phase), "r"(ns)
+            : "memory");
+    }
+}
 // non-blocking probe of a phase (the issuer polls several barriers)
 __device__ __forceinline__ bool mbar_test(uint64_t *bar, uint32_t phase) {
     uint32_t ok;

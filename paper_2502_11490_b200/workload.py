@@ -167,7 +167,7 @@ def exact_graph(name: str, items, m: int, rank: int = 0) -> GraphIndex:
     probe = items[:: max(1, N // 8192)].double().cpu().numpy()
     key = hashlib.sha256(probe.tobytes()).hexdigest()[:16]
     cache = os.environ.get("GMPGR_CACHE", "/tmp/gmpgr_cache")
-    path = os.path.join(cache, f"{name}_{N}x{d}_m{m}_ef64_{key}.npz")
+    path = os.path.join(cache, f"{name}_{N}x{d}_m{m}_ef64_{key}_v2.npz")
     if not os.path.exists(path):
         if rank == 0:
             index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
@@ -175,8 +175,9 @@ def exact_graph(name: str, items, m: int, rank: int = 0) -> GraphIndex:
             os.makedirs(cache, exist_ok=True)
             arrs = {"ids": ids, "levels": levels, "entry": np.int64(entry), "m": np.int64(index.m),
                     "max_layers": np.int64(index.max_layers)}
-            for l, (nb, ct) in enumerate(layers):
-                arrs[f"nb{l}"], arrs[f"ct{l}"] = nb, ct
+            for l, (nb, ct) in enumerate(layers):  # upper layers: member rows only
+                rows = np.arange(N) if l == 0 else np.nonzero(levels[:N] >= l)[0]
+                arrs[f"rows{l}"], arrs[f"nb{l}"], arrs[f"ct{l}"] = rows, nb[rows], ct[rows]
             tmp = path + f".tmp{os.getpid()}.npz"
             np.savez(tmp, **arrs)
             os.replace(tmp, path)
@@ -188,8 +189,15 @@ def exact_graph(name: str, items, m: int, rank: int = 0) -> GraphIndex:
             time.sleep(2.0)
     z = np.load(path)
     nl = sum(1 for f in z.files if f.startswith("nb"))
-    return GraphIndex.from_arrays(z["ids"], z["levels"], [(z[f"nb{l}"], z[f"ct{l}"]) for l in range(nl)],
-                                  int(z["entry"]), m=int(z["m"]), max_layers=int(z["max_layers"]))
+    layers = []
+    for l in range(nl):
+        rows, nbm, ctm = z[f"rows{l}"], z[f"nb{l}"], z[f"ct{l}"]
+        nb = np.zeros((N, nbm.shape[1]), dtype=np.int32)
+        ct = np.zeros(N, dtype=np.int32)
+        nb[rows], ct[rows] = nbm, ctm
+        layers.append((nb, ct))
+    return GraphIndex.from_arrays(z["ids"], z["levels"], layers, int(z["entry"]), m=int(z["m"]),
+                                  max_layers=int(z["max_layers"]))
 
 
 def make_shard(rank: int, world: int, shard_n: int = 12_500_000, d: int = 128, m: int = 24,
