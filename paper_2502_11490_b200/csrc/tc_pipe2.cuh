@@ -161,7 +161,10 @@ struct TcPipe2 {
                         continue;
                     }
                 }
-                if (l0t < T) {
+                // a pending layer 1 goes first: the next tile's layer 0 starts only once every
+                // earlier layer 1 is issued, so the epilogue's layer-1 round trip never queues
+                // behind 24 layer-0 MMAs (those then run under the epilogue's layer-1 work)
+                if (l0t < T && !(l1t < l0t && l0k == 0)) {
                     const uint32_t tg = tile_ctr + l0t, b = tg & 1u, use = tg >> 1;
                     const uint32_t qg = chunk_ctr + l0t * NC + l0k, s = qg % S, r = qg / S;
                     // D0 buffer b must have been read by the epilogue (two tiles back)
