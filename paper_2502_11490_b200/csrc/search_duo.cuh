@@ -229,27 +229,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if constexpr (MODE == 1) {
-        tmem = *tptr + unit * TP::COLS;
-        // collapsed heads for the tensor-core epilogue: w_eff = sum_o att_o W2_o, c0 =
-        // sum_o att_o b2_o, hlim = largest relu output for which no head can overflow
-        float *weff = satt + 4;
-        if (lt < 64) {
-            float w = 0.f;
-            for (int o = 0; o < ZZ; ++o) w = fmaf(satt[o], sW2[o * 64 + lt], w);
-            weff[lt] = w;
-        } else if (lt == 64) {
-            float c0 = 0.f, hl = 3.0e38f;
-            for (int o = 0; o < ZZ; ++o) {
-                c0 = fmaf(satt[o], sb2[o], c0);
-                float l1 = 0.f;
-                for (int j = 0; j < 64; ++j) l1 += fabsf(sW2[o * 64 + j]);
-                hl = fminf(hl, (1.0e37f - fabsf(sb2[o])) / fmaxf(l1, 1e-30f));
-            }
-            weff[64] = c0;
-            weff[65] = hl;
-        }
-    }
+    if constexpr (MODE == 1) tmem = *tptr + unit * TP::COLS;
 
     MqState<G> &st = sts[unit];
     int *nlog = nlog_[unit];
@@ -285,7 +265,6 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     const int top = g.n_layers - 1, nst = 5 + g.n_layers, d_h = DH;
 
     for (;;) {
-        if ((a.exp & 64) && unit == 1) break;  // experiment: one active unit per SM
         usync();
         if (lt == 0) st.base = atomicAdd(a.queue, G);
         usync();
@@ -332,10 +311,10 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
 
         // ================= helpers
         auto score_fresh = [&](int n, int layer, int hop) {
-            auto on_score = [&](int i, bool valid, float v, int gq, int32_t s, uint32_t rank) {
+            auto on_score = [&](int i, bool valid, float v, int gq, int32_t s) {
                 // i: physical index of the fresh claim; evaluations are counted by expand
                 if (valid && !isfinite(v)) atomicOr(a.nonfinite, 1);
-                const uint64_t key = make_key(v, rank);
+                const uint64_t key = make_key(v, slot_rank(g, s));
                 if (valid) fr_key[i] = key;
                 MqQuery &Q = st.qs[gq];
                 bool app;
@@ -387,8 +366,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         const bool valid = lt < nv;
                         int egq = 0, eph = 0;
                         if (valid) fresh_at(base + lt, egq, eph);
-                        const int32_t es = valid ? fr_v[eph] : 0;
-                        on_score(eph, valid, valid ? sc[lt] : 0.f, egq, es, slot_rank(g, es));
+                        on_score(eph, valid, valid ? sc[lt] : 0.f, egq, valid ? fr_v[eph] : 0);
                     }
                     usync();
                 }
