@@ -1019,12 +1019,11 @@ int launch_mq(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_ite
 }
 
 // ------------------------------------------------------------------ duo kernel
-// bytes of duo scratch per unit: frontier lists (2 x slot + searcher), per-query fresh-claim
-// regions (slot, key, exact flag) + re-score requests, per-query pools / bitsets / logs
+// bytes of duo scratch per unit (lists x G queries, hash, per-query pools / bitsets / logs)
 size_t duo_unit_bytes(int64_t G, int64_t capF, int64_t capS, int64_t capP, int64_t hcap, int64_t vwords,
                       int64_t logcap) {
     const int64_t lF = capF * G, lS = capS * G;
-    return (size_t)(2 * 2 * lF * 4 + 3 * lS * 4 + lS * 8 + hcap * 8 + G * 2 * capP * 16 + G * vwords * 4 +
+    return (size_t)(2 * 2 * lF * 4 + 5 * lS * 4 + 2 * lS * 8 + hcap * 8 + G * 2 * capP * 16 + G * vwords * 4 +
                     G * logcap * 4);
 }
 
@@ -1039,10 +1038,11 @@ int ensure_duo_scratch(gr_searcher *S, int64_t units, int64_t G, int64_t capF, i
     int rc = GR_OK;
     if ((rc = dmalloc(&D.f_slot, (size_t)units * 2 * lF))) return rc;
     if ((rc = dmalloc(&D.f_srch, (size_t)units * 2 * lF))) return rc;
-    int32_t **lists[] = {&D.surv_v, &D.cont_v, &D.cont_i};  // fresh slots, re-score requests, exact flags
+    int32_t **lists[] = {&D.surv_v, &D.surv_i, &D.cont_v, &D.cont_i, &D.seg_v};
     for (int32_t **l : lists)
         if ((rc = dmalloc(l, (size_t)units * lS))) return rc;
     if ((rc = dmalloc(&D.fr_key, (size_t)units * lS))) return rc;
+    if ((rc = dmalloc(&D.seg_key, (size_t)units * lS))) return rc;
     if (hcap && (rc = dmalloc(&D.hash, (size_t)units * hcap))) return rc;
     if ((rc = dmalloc(&D.pool_key, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&D.pool_slot, (size_t)slots * 2 * capP))) return rc;
@@ -1197,9 +1197,12 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     a.f_slot = D.f_slot;
     a.f_srch = D.f_srch;
     a.surv_v = D.surv_v;
+    a.surv_i = D.surv_i;
     a.cont_v = D.cont_v;
     a.cont_i = D.cont_i;
     a.fr_key = D.fr_key;
+    a.seg_v = D.seg_v;
+    a.seg_key = D.seg_key;
     a.pool_key = D.pool_key;
     a.pool_slot = D.pool_slot;
     a.pool_meta = D.pool_meta;

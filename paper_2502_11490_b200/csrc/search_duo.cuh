@@ -170,7 +170,6 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     __shared__ unsigned long long ph_acc[16];
     __shared__ unsigned bc[2];  // tensor-core band certificate (band_record)
     __shared__ int nlog_[2][G];
-    __shared__ int nq_[2][G], qoff_[2][G + 1];  // fresh claims per query this hop, virtual offsets
     const int tid = threadIdx.x, unit = tid >> 8, lt = tid & 255, warp = lt >> 5, lane = lt & 31;
     if (tid < 16) ph_acc[tid] = 0;
     if (tid < 2) bc[tid] = 0u;
@@ -233,29 +232,21 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
 
     MqState<G> &st = sts[unit];
     int *nlog = nlog_[unit];
-    int *nq = nq_[unit], *qoff = qoff_[unit];
     // ---- scratch: unit-level flattened lists, per-query visited bitsets / logs / pools
     const int64_t ug = (int64_t)blockIdx.x * 2 + unit;  // global unit index
     const int64_t capF = a.capF, capS = a.capS, capP = a.capP;  // lists already x G
     int32_t *fslot[2] = {a.f_slot + ug * 2 * capF, a.f_slot + ug * 2 * capF + capF};
     int32_t *fsrch[2] = {a.f_srch + ug * 2 * capF, a.f_srch + ug * 2 * capF + capF};
-    // this hop's fresh claims (= survivors of expand) live in per-query regions of capQ
-    // entries, in the query's searcher order: every (query, searcher) segment is a
-    // contiguous range, counted by the owning warp during expand (no grouping pass).
-    // Scoring walks them as one virtual list [0, nFresh) through the per-query offsets.
-    const int64_t capQ = capS / G;
-    int32_t *fr_v = a.surv_v + ug * capS;       // [G][capQ] slots
-    uint64_t *fr_key = a.fr_key + ug * capS;    // [G][capQ] keys (physical index)
-    int32_t *rq = a.cont_v + ug * capS;         // re-score requests (gq << 24 | physical index)
-    int32_t *seg_ex = a.cont_i + ug * capS;     // [G][capQ] exact-rescored flags
-    // virtual fresh-claim index -> (query, physical index)
-    auto fresh_at = [&](int i, int &gq, int &phys) {
-        int q = 0;
-#pragma unroll
-        for (int j = 1; j < G; ++j) q += i >= qoff[j];
-        gq = q;
-        phys = (int)(q * capQ) + (i - qoff[q]);
-    };
+    int32_t *surv_v = a.surv_v + ug * capS, *surv_i = a.surv_i + ug * capS;
+    int32_t *cont_v = a.cont_v + ug * capS, *cont_i = a.cont_i + ug * capS;
+    // fresh claims ARE the survivors (unique per (query, node)); their searcher field is
+    // lowered to the lowest toucher by the resolve pass before the frontier split reads it
+    int32_t *fr_v = surv_v, *fr_i = surv_i;
+    uint64_t *fr_key = a.fr_key + ug * capS;
+    int32_t *seg_v = a.seg_v + ug * capS;
+    uint64_t *seg_key = a.seg_key + ug * capS;
+    int32_t *rq = cont_v;      // re-score requests (gq << 24 | index); contested lists are dead
+    int32_t *seg_ex = cont_i;  // after resolve
     auto vis_of = [&](int gq) { return a.vis + (ug * G + gq) * a.vis_words; };
     auto log_of = [&](int gq) { return a.vlog + (ug * G + gq) * (int64_t)a.log_cap; };
     auto pkey = [&](int gq, int c) { return a.pool_key + ((ug * G + gq) * 2 + c) * capP; };
@@ -311,8 +302,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
 
         // ================= helpers
         auto score_fresh = [&](int n, int layer, int hop) {
-            auto on_score = [&](int i, bool valid, float v, int gq, int32_t s) {
-                // i: physical index of the fresh claim; evaluations are counted by expand
+            auto on_score = [&](int i, bool valid, float v, int gi, int32_t s) {
+                const int gq = gi >> 16;  // evaluations are counted per query by expand
                 if (valid && !isfinite(v)) atomicOr(a.nonfinite, 1);
                 const uint64_t key = make_key(v, slot_rank(g, s));
                 if (valid) fr_key[i] = key;
@@ -332,11 +323,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 }
             };
             if constexpr (MODE == 1) {
-                auto entry = [&](int i, int32_t &slot, int &gq, int &phys) {
-                    fresh_at(i, gq, phys);
-                    slot = fr_v[phys];
-                };
-                TP::run(smem, ub, U, sb1, sW2, sb2, satt, tmem, a.it, g, entry, n, chunk_ctr, tile_ctr, lt,
+                TP::run(smem, ub, U, sb1, sW2, sb2, satt, tmem, a.it, g, fr_v, fr_i, n, chunk_ctr, tile_ctr, lt,
                         on_score, usync, &a.hl_map,
                         a.phase_cycles && unit == 0 ? ph_acc + 8 : nullptr, a.exp);
                 if (lt == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
@@ -348,25 +335,22 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     for (int pp = 0; pp < 4; ++pp) {
                         const int p = warp * 4 + pp;
                         float4 *xr = sBuf + EX::OFF_X0 + p * EX::LDX0;
-                        int pgq = 0, pph = 0;
                         if (p < nv) {
-                            fresh_at(base + p, pgq, pph);
                             const float4 *hv = reinterpret_cast<const float4 *>(
-                                a.it.emb + slot_row(g, fr_v[pph]) * a.it.ld);
+                                a.it.emb + slot_row(g, fr_v[base + p]) * a.it.ld);
                             for (int cc = lane; cc < DH / 4; cc += 32)
                                 xr[chunk_perm(DH / 4 + cc, 2 * DH) - DH / 4] = __ldg(hv + cc);
                         } else {
                             for (int cc = lane; cc < DH / 4; cc += 32) xr[cc] = make_float4(0.f, 0.f, 0.f, 0.f);
                         }
-                        if (lane == 0) pq[p] = pgq;
+                        if (lane == 0) pq[p] = p < nv ? (fr_i[base + p] >> 16) : 0;
                     }
                     usync();
                     EX::tile(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync);
                     if (lt < 32) {
                         const bool valid = lt < nv;
-                        int egq = 0, eph = 0;
-                        if (valid) fresh_at(base + lt, egq, eph);
-                        on_score(eph, valid, valid ? sc[lt] : 0.f, egq, valid ? fr_v[eph] : 0);
+                        on_score(base + lt, valid, valid ? sc[lt] : 0.f, valid ? fr_i[base + lt] : 0,
+                                 valid ? fr_v[base + lt] : 0);
                     }
                     usync();
                 }
@@ -386,7 +370,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         if (p < nv) {
                             const int e = rq[base + p];
                             const int gq = e >> 24, idx = e & 0xFFFFFF;
-                            const int32_t s = pool ? pslot(gq, st.qs[gq].pool_cur)[idx] : fr_v[idx];
+                            const int32_t s = pool ? pslot(gq, st.qs[gq].pool_cur)[idx] : seg_v[idx];
                             const float4 *hv = reinterpret_cast<const float4 *>(a.it.emb + slot_row(g, s) * a.it.ld);
                             for (int cc = lane; cc < DH / 4; cc += 32)
                                 xr[chunk_perm(DH / 4 + cc, 2 * DH) - DH / 4] = __ldg(hv + cc);
@@ -401,14 +385,14 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     if (lt < nv) {
                         const int e = rq[base + lt];
                         const int gq = e >> 24, idx = e & 0xFFFFFF;
-                        band_record(bc, pool ? pkey(gq, st.qs[gq].pool_cur)[idx] : fr_key[idx], sc[lt],
+                        band_record(bc, pool ? pkey(gq, st.qs[gq].pool_cur)[idx] : seg_key[idx], sc[lt],
                                     a.band_rel, a.band_abs);
                         if (pool) {
                             const int c = st.qs[gq].pool_cur;
                             pkey(gq, c)[idx] = make_key(sc[lt], slot_rank(g, pslot(gq, c)[idx]));
                             pmeta(gq, c)[idx] |= 1;
                         } else {
-                            fr_key[idx] = make_key(sc[lt], slot_rank(g, fr_v[idx]));
+                            seg_key[idx] = make_key(sc[lt], slot_rank(g, seg_v[idx]));
                             seg_ex[idx] = 1;
                         }
                     }
@@ -480,23 +464,9 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
         };
         // this hop's first touches [0, nS) are the fresh claims (already in the visited bits and
         // in their query's claim log, written by the owning warp during expand)
-        auto resolve = [&]() {
-            if (lt == 0) {
-                int o = 0;
-                for (int q = 0; q < G; ++q) { qoff[q] = o; o += nq[q]; }
-                qoff[G] = o;
-                st.nFresh = o;
-            }
+        auto resolve = [&](int nS) {
+            if (lt == 0) st.nFresh = nS;
             usync();
-        };
-        // append v (when ok) to query w's fresh-claim region; called by warp w
-        auto fresh_push = [&](int w, bool ok, int32_t v) {
-            const unsigned m = __ballot_sync(0xffffffffu, ok);
-            const int p = nq[w] + __popc(m & ((1u << lane) - 1u));
-            if (ok) fr_v[w * capQ + p] = v;
-            __syncwarp();
-            if (lane == 0) nq[w] += __popc(m);
-            __syncwarp();
         };
         // append v (when ok) to query w's claim log; called by warp w (the only writer of nlog[w])
         auto log_push = [&](int w, bool ok, int32_t v) {
@@ -520,13 +490,13 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
 
         // ================= init: entry + its top-layer neighbourhood (hop 0), as first
         // touches of searcher 0 (the entry's row never contains the entry)
-        if (lt == 0) st.nFresh = 0;
-        if (lt < G) nq[lt] = 0;
+        if (lt == 0) { st.nS = 0; st.nFresh = 0; }
         usync();
         if (lt < G && st.qs[lt].q >= 0) {
+            const int idx = atomicAdd(&st.nS, 1);
             atomicOr(vis_of(lt) + (g.entry >> 5), 1u << (g.entry & 31));
-            fr_v[lt * capQ] = g.entry;
-            nq[lt] = 1;
+            surv_v[idx] = g.entry;
+            surv_i[idx] = lt << 16;
             log_of(lt)[0] = g.entry;
             nlog[lt] = 1;
         }
@@ -542,14 +512,14 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     if (lane == 0) st.qs[warp].nbrs += nv;
                     uint32_t s2 = 1u;
                     if (v >= 0) s2 = (atomicOr(vb + (v >> 5), 1u << (v & 31)) >> (v & 31)) & 1u;
-                    fresh_push(warp, v >= 0 && s2 == 0u, v);
+                    warp_append2(v >= 0 && s2 == 0u, v, warp << 16, &st.nS, surv_v, surv_i);
                     log_push(warp, v >= 0 && s2 == 0u, v);
                 }
             }
             if (lane == 0) st.qs[warp].per_layer[top] = nlog[warp];  // entry + fresh neighbours
         }
         usync();
-        resolve();
+        resolve(st.nS);
         score_fresh(st.nFresh, top, 0);
         compact_pools();
         GR_PH(0);
@@ -600,9 +570,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 const int nF = st.nF;
                 if (nF == 0) { h += a.hops - 1 - t; break; }
                 const int fc = st.f_cur;
-                if (lt == 0) st.nFresh = 0;
-                if (lt < G) nq[lt] = 0;
-                for (int i = lt; i < NSEG; i += NTH) seg_cnt[i] = 0;
+                if (lt == 0) { st.nS = 0; st.nFresh = 0; }
                 usync();
                 // ---- expand + claim: warp w owns query w and walks its frontier in list order
                 // (searcher-ascending) in batches of <= RW rows of ONE searcher; a batch's 16-byte
@@ -673,7 +641,6 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     int4 pv[3];
                     int e0 = st.qs[warp].f_off;
                     int lbase = nlog[warp];  // this query's claim log (warp-private during expand)
-                    int rc = 0;              // this query's fresh claims this hop
                     int32_t *const lg = log_of(warp);
                     int32_t gi = meta(e0, ms, len);
                     pieces(ms, pv);
@@ -709,20 +676,20 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const int ys = __shfl_up_sync(FULL, is, o);
                             if (lane >= o) is += ys;
                         }
-                        const int tot = __shfl_sync(FULL, is, 31);
-                        int bs = rc + is - cs;  // this query's region, in searcher order
+                        int bs = 0;
+                        if (lane == 31 && is) bs = atomicAdd(&st.nS, is);
+                        bs = __shfl_sync(FULL, bs, 31) + is - cs;
                         int lp = lbase + is - cs;
-                        lbase += tot;
-                        rc += tot;
-                        if (lane == 0 && tot) seg_cnt[warp * a.kp + (gi & 0xFFFF)] += tot;  // one searcher per batch
+                        lbase += __shfl_sync(FULL, is, 31);
 #pragma unroll
                         for (int j = 0; j < 3; ++j) {
                             const int vv[4] = {pv[j].x, pv[j].y, pv[j].z, pv[j].w};
 #pragma unroll
                             for (int u = 0; u < 4; ++u)
                                 if (vv[u] >= 0 && s2[j][u] == 0u) {
-                                    GR_DCHECK(bs < capQ && vv[u] < g.n, "survivor %d cap %lld v %d", bs, (long long)capQ, vv[u]);
-                                    fr_v[warp * capQ + bs] = vv[u];
+                                    GR_DCHECK(bs < capS && vv[u] < g.n, "survivor %d cap %lld v %d", bs, (long long)capS, vv[u]);
+                                    surv_v[bs] = vv[u];
+                                    surv_i[bs] = gi;
                                     ++bs;
                                     if (lp < a.log_cap) lg[lp] = vv[u];
                                     ++lp;
@@ -742,14 +709,13 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     if (lane == 0) {
                         st.qs[warp].rows += nrows;
                         st.qs[warp].nbrs += nnbr;
-                        st.qs[warp].per_layer[layer] += rc;  // this hop's evaluations
+                        st.qs[warp].per_layer[layer] += lbase - nlog[warp];  // this hop's evaluations
                         nlog[warp] = lbase;
-                        nq[warp] = rc;
                     }
                 }
                 usync();
                 GR_PH(2);
-                resolve();
+                resolve(st.nS);
                 GR_PH(3);
                 const int nFresh = st.nFresh;
                 score_fresh(nFresh, layer, h);
@@ -757,8 +723,18 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                 compact_pools();
                 GR_PH(5);
                 if (t == a.hops - 1) break;
-                // ---- per-(query, searcher) top-ef of fresh claims -> next frontier; segment
-                // (q, s) is the range [seg_off, + seg_cnt) of query q's region (counted by expand)
+                // ---- per-(query, searcher) top-ef of fresh claims -> next frontier
+                for (int i = lt; i < NSEG; i += NTH) seg_cnt[i] = 0;
+                usync();
+                auto seg_of = [&](int gi) { return (gi >> 16) * a.kp + (gi & 0xFFFF); };
+                for (int t0 = 0; t0 < nFresh; t0 += NTH) {
+                    const int t2 = t0 + lt;
+                    if (t0 + warp * 32 < nFresh) {
+                        const int sg = t2 < nFresh ? seg_of(fr_i[t2]) : 0;
+                        warp_count(&seg_cnt[sg], sg, 1, t2 < nFresh);
+                    }
+                }
+                usync();
                 if (warp == 0) {  // exclusive scans of counts and min(count, ef)
                     int acc = 0, accf = 0;
                     for (int i0 = 0; i0 < NSEG; i0 += 32) {
@@ -770,11 +746,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const int y = __shfl_up_sync(0xffffffffu, x, o), yf = __shfl_up_sync(0xffffffffu, xf, o);
                             if (lane >= o) { x += y; xf += yf; }
                         }
-                        if (i < NSEG) {
-                            const int q = i / a.kp;  // query q's segments sum to nq[q]: in-region offset
-                            seg_off[i] = (int)(q * capQ) + (acc + x - c - qoff[q]);
-                            fn_off[i] = accf + xf - cf;
-                        }
+                        if (i < NSEG) { seg_off[i] = acc + x - c; fn_off[i] = accf + xf - cf; seg_cnt[i] = 0; }
                         acc += __shfl_sync(0xffffffffu, x, 31);
                         accf += __shfl_sync(0xffffffffu, xf, 31);
                     }
@@ -787,23 +759,26 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     }
                 }
                 usync();
+                for (int t2 = lt; t2 < nFresh; t2 += NTH) {
+                    const int sg = seg_of(fr_i[t2]);
+                    const int pos = seg_off[sg] + atomicAdd(&seg_cnt[sg], 1);
+                    seg_v[pos] = fr_v[t2];
+                    seg_key[pos] = fr_key[t2];
+                }
+                usync();
                 if constexpr (MODE == 1) {
-                    for (int t2 = lt; t2 < nFresh; t2 += NTH) {
-                        int q2, ph2;
-                        fresh_at(t2, q2, ph2);
-                        seg_ex[ph2] = 0;
-                    }
+                    for (int t2 = lt; t2 < nFresh; t2 += NTH) seg_ex[t2] = 0;
                     if (lt == 0) st.nRq = 0;
                     usync();
                     for (int sg = warp; sg < NSEG; sg += NW) {
                         const int ni = seg_cnt[sg], off = seg_off[sg], gq = sg / a.kp;
                         if (ni <= a.ef) continue;
-                        const uint64_t Ta = warp_select_threshold(fr_key + off, ni, a.ef, hist + warp * 256);
+                        const uint64_t Ta = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
                         const float Ts = orderable_f32((uint32_t)(Ta >> 32)), bd = band_of(Ts);
                         for (int j0 = 0; j0 < ni; j0 += 32) {
                             const int j = j0 + lane;
                             const bool in = j < ni &&
-                                fabsf(orderable_f32((uint32_t)(fr_key[off + j] >> 32)) - Ts) <= bd;
+                                fabsf(orderable_f32((uint32_t)(seg_key[off + j] >> 32)) - Ts) <= bd;
                             warp_append1(in, (gq << 24) | (off + j), &st.nRq, rq);
                         }
                     }
@@ -816,17 +791,17 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     const int gi = ((sg / a.kp) << 16) | (sg % a.kp);
                     if (ni <= a.ef) {
                         GR_DCHECK(fo + ni <= capF, "frontier write %d + %d > %lld", fo, ni, (long long)capF);
-                        for (int j = lane; j < ni; j += 32) { fslot[fn][fo + j] = fr_v[off + j]; fsrch[fn][fo + j] = gi; }
+                        for (int j = lane; j < ni; j += 32) { fslot[fn][fo + j] = seg_v[off + j]; fsrch[fn][fo + j] = gi; }
                     } else {
-                        const uint64_t T = warp_select_threshold(fr_key + off, ni, a.ef, hist + warp * 256);
+                        const uint64_t T = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
                         int cnt = 0;
                         for (int j0 = 0; j0 < ni; j0 += 32) {
                             const int j = j0 + lane;
-                            const bool keep = j < ni && fr_key[off + j] >= T;
+                            const bool keep = j < ni && seg_key[off + j] >= T;
                             const unsigned mask = __ballot_sync(0xffffffffu, keep);
                             if (keep) {
                                 const int pos = fo + cnt + __popc(mask & ((1u << lane) - 1u));
-                                fslot[fn][pos] = fr_v[off + j];
+                                fslot[fn][pos] = seg_v[off + j];
                                 fsrch[fn][pos] = gi;
                             }
                             cnt += __popc(mask);

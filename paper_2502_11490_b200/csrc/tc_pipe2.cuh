@@ -64,17 +64,17 @@ struct TcPipe2 {
         }
     }
 
-    // Score pairs [0, n) of this unit: entry(i, slot, gq, idx) names pair i's item slot, its
-    // query and the caller's storage index.  Every epilogue thread calls
-    // on_score(idx, valid, score, gq, slot) per row (all 32 lanes of its warp together).  sm: CTA carve base (weights); u: this unit's
+    // Score pairs [0, n) of this unit: item slot slots[i], pair tag gis[i] (query << 16 |
+    // searcher).  Every epilogue thread calls on_score(i, valid, score, gi, slot) per row
+    // (all 32 lanes of its warp together).  sm: CTA carve base (weights); u: this unit's
     // block; misc: U [G][64] (user half + b0), b1[64], W2[Z][64], b2[4], att[4] (shared
     // memory); tmem: this unit's TMEM window; chunk_ctr / tile_ctr: unit-lifetime counters;
     // sync(): the unit's barrier.
-    template <class Entry, class OnScore, class Sync>
+    template <class OnScore, class Sync>
     static __device__ __forceinline__ void run(unsigned char *sm, unsigned char *u, const float *U,
                                                const float *b1, const float *W2, const float *b2,
                                                const float *att, uint32_t tmem, const DevItems &it,
-                                               const DevGraph &g, Entry entry,
+                                               const DevGraph &g, const int32_t *slots, const int32_t *gis,
                                                int n, uint32_t &chunk_ctr, uint32_t &tile_ctr, int lt,
                                                OnScore on_score, Sync sync, const void *tmap,
                                                unsigned long long *tmr = nullptr, int exp = 0) {
@@ -99,11 +99,7 @@ struct TcPipe2 {
 #pragma unroll
                     for (int j = 0; j < 4; ++j) {
                         const int r = 4 * grp + j;
-                        int32_t sl = -1;
-                        if (r < nv) {
-                            int eq, ei;
-                            entry(base + r, sl, eq, ei);
-                        }
+                        const int32_t sl = r < nv ? slots[base + r] : -1;
                         dst[j] = sl < 0 ? 0 : (it.hl_by_slot ? (int)sl : (int)slot_row(g, sl));
                     }
                 };
@@ -211,9 +207,8 @@ struct TcPipe2 {
             for (int t = 0; t < T; ++t) {
                 const uint32_t tg = tile_ctr + t;
                 const int base = t * TM, nv = min(TM, n - base);
-                int32_t my_s = 0;
-                int gq = 0, my_i = 0;
-                if (row < nv) entry(base + row, my_s, gq, my_i);
+                const int gi = row < nv ? gis[base + row] : 0, gq = gi >> 16;
+                const int32_t my_s = row < nv ? slots[base + row] : 0;
                 const float *uq = U + gq * H;
                 const uint32_t b = tg & 1u;
                 long long c0 = et ? clock64() : 0;
@@ -281,7 +276,7 @@ struct TcPipe2 {
                     bad |= !isfinite(z);
                     s = fmaf(z, att[o], s);
                 }
-                on_score(my_i, row < nv, bad ? __int_as_float(0x7fc00000) : s, gq, my_s);
+                on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s, gi, my_s);
                 if (et) tmr[1] += clock64() - c0;
             }
             if (et) tmr[4] += clock64() - e_start;
