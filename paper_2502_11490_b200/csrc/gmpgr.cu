@@ -1093,7 +1093,7 @@ int plan_duo(int k, int kp, SearchArgs &a) {
     a.off_hist = place(hist_b);
     a.off_sortk = place(sortk_b);
     a.off_sortv = place(sortv_b);
-    a.off_misc = U.alloc((G * 64 + 64 + 64 * ZZ + 8) * 4);
+    a.off_misc = U.alloc((G * 64 + 64 + 64 * ZZ + 8 + 64 + 4) * 4);  // + w_eff, c0, hlim
     a.off_acc0 = U.alloc(G * 64 * 16);
     a.off_kp = U.alloc(3 * G * kp * 4);
     a.unit_stride = up(U.bytes, 1024);

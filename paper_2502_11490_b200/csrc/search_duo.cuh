@@ -228,7 +228,27 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     tc::fence_before();
     __syncthreads();
     tc::fence_after();
-    if constexpr (MODE == 1) tmem = *tptr + unit * TP::COLS;
+    if constexpr (MODE == 1) {
+        tmem = *tptr + unit * TP::COLS;
+        // collapsed heads for the tensor-core epilogue: w_eff = sum_o att_o W2_o, c0 =
+        // sum_o att_o b2_o, hlim = largest relu output for which no head can overflow
+        float *weff = satt + 4;
+        if (lt < 64) {
+            float w = 0.f;
+            for (int o = 0; o < ZZ; ++o) w = fmaf(satt[o], sW2[o * 64 + lt], w);
+            weff[lt] = w;
+        } else if (lt == 64) {
+            float c0 = 0.f, hl = 3.0e38f;
+            for (int o = 0; o < ZZ; ++o) {
+                c0 = fmaf(satt[o], sb2[o], c0);
+                float l1 = 0.f;
+                for (int j = 0; j < 64; ++j) l1 += fabsf(sW2[o * 64 + j]);
+                hl = fminf(hl, (1.0e37f - fabsf(sb2[o])) / fmaxf(l1, 1e-30f));
+            }
+            weff[64] = c0;
+            weff[65] = hl;
+        }
+    }
 
     MqState<G> &st = sts[unit];
     int *nlog = nlog_[unit];
@@ -302,10 +322,10 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
 
         // ================= helpers
         auto score_fresh = [&](int n, int layer, int hop) {
-            auto on_score = [&](int i, bool valid, float v, int gi, int32_t s) {
+            auto on_score = [&](int i, bool valid, float v, int gi, int32_t s, uint32_t rank) {
                 const int gq = gi >> 16;  // evaluations are counted per query by expand
                 if (valid && !isfinite(v)) atomicOr(a.nonfinite, 1);
-                const uint64_t key = make_key(v, slot_rank(g, s));
+                const uint64_t key = make_key(v, rank);
                 if (valid) fr_key[i] = key;
                 MqQuery &Q = st.qs[gq];
                 bool app;
@@ -349,8 +369,9 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     EX::tile(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync);
                     if (lt < 32) {
                         const bool valid = lt < nv;
-                        on_score(base + lt, valid, valid ? sc[lt] : 0.f, valid ? fr_i[base + lt] : 0,
-                                 valid ? fr_v[base + lt] : 0);
+                        const int32_t es = valid ? fr_v[base + lt] : 0;
+                        on_score(base + lt, valid, valid ? sc[lt] : 0.f, valid ? fr_i[base + lt] : 0, es,
+                                 slot_rank(g, es));
                     }
                     usync();
                 }

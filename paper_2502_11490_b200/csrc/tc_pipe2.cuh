@@ -65,10 +65,10 @@ struct TcPipe2 {
     }
 
     // Score pairs [0, n) of this unit: item slot slots[i], pair tag gis[i] (query << 16 |
-    // searcher).  Every epilogue thread calls on_score(i, valid, score, gi, slot) per row
+    // searcher).  Every epilogue thread calls on_score(i, valid, score, gi, slot, rank) per row
     // (all 32 lanes of its warp together).  sm: CTA carve base (weights); u: this unit's
-    // block; misc: U [G][64] (user half + b0), b1[64], W2[Z][64], b2[4], att[4] (shared
-    // memory); tmem: this unit's TMEM window; chunk_ctr / tile_ctr: unit-lifetime counters;
+    // block; misc: U [G][64] (user half + b0), b1[64], W2[Z][64], b2[4], att[4], w_eff[64],
+    // c0, hlim (shared memory); tmem: this unit's TMEM window; chunk_ctr / tile_ctr: unit-lifetime counters;
     // sync(): the unit's barrier.
     template <class OnScore, class Sync>
     static __device__ __forceinline__ void run(unsigned char *sm, unsigned char *u, const float *U,
@@ -209,6 +209,8 @@ struct TcPipe2 {
                 const int base = t * TM, nv = min(TM, n - base);
                 const int gi = row < nv ? gis[base + row] : 0, gq = gi >> 16;
                 const int32_t my_s = row < nv ? slots[base + row] : 0;
+                // the tie-break rank is loaded here, under the tile's MMA waits, not after the heads
+                const uint32_t my_rank = slot_rank(g, my_s);
                 const float *uq = U + gq * H;
                 const uint32_t b = tg & 1u;
                 long long c0 = et ? clock64() : 0;
@@ -245,38 +247,58 @@ struct TcPipe2 {
                 tc::mbar_wait(bar(u, D1FULL), tg & 1u);
                 if (et) { const long long c = clock64(); tmr[3] += c - c0; c0 = c; }
                 tc::fence_after();
+                int hmax_bits;
                 {
                     tc::tmem_ld64(tmem + lanebase + C_D1, h);
+                    // relu; the integer max of the pre-activation bit patterns is the largest
+                    // relu output (negative values have the sign bit set) and catches NaN / +inf
+                    int hbits = 0;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) h[j] = fmaxf(h[j] + b1[j], 0.f);
+                    for (int j = 0; j < 64; ++j) {
+                        const float x = h[j] + b1[j];
+                        hbits = max(hbits, __float_as_int(x));
+                        h[j] = fmaxf(x, 0.f);
+                    }
+                    hmax_bits = hbits;
                 }
                 tc::fence_before();
                 // approximate path (reassociated): the exact refinement re-scores every item
-                // near a threshold, and the band certificate checks the error at run time
+                // near a threshold, and the band certificate checks the error at run time.
+                // Heads + attention are linear: score = c0 + h . w_eff (w_eff = sum_o att_o W2_o,
+                // c0 = sum_o att_o b2_o) whenever no head can overflow (max h < hlim); otherwise
+                // the heads are evaluated one by one for the reference's non-finite check.
                 float s = 0.f;
                 bool bad = false;
-                const float4 *W2v = reinterpret_cast<const float4 *>(W2);
-                float zp[Z][4];
+                const float *weff = att + 4;  // [64] w_eff, then c0, hlim
+                if (hmax_bits < __float_as_int(weff[65])) {
+                    const float4 *wv = reinterpret_cast<const float4 *>(weff);
+                    float sp[4] = {0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-                for (int o = 0; o < Z; ++o) zp[o][0] = zp[o][1] = zp[o][2] = zp[o][3] = 0.f;
-#pragma unroll
-                for (int j = 0; j < 64; j += 4) {
-#pragma unroll
+                    for (int j = 0; j < 64; j += 4) {
+                        const float4 w = wv[j / 4];
+                        sp[0] = fmaf(h[j], w.x, sp[0]);
+                        sp[1] = fmaf(h[j + 1], w.y, sp[1]);
+                        sp[2] = fmaf(h[j + 2], w.z, sp[2]);
+                        sp[3] = fmaf(h[j + 3], w.w, sp[3]);
+                    }
+                    s = weff[64] + ((sp[0] + sp[1]) + (sp[2] + sp[3]));
+                } else {
+                    const float4 *W2v = reinterpret_cast<const float4 *>(W2);
                     for (int o = 0; o < Z; ++o) {
-                        const float4 w = W2v[o * (H / 4) + j / 4];
-                        zp[o][0] = fmaf(h[j], w.x, zp[o][0]);
-                        zp[o][1] = fmaf(h[j + 1], w.y, zp[o][1]);
-                        zp[o][2] = fmaf(h[j + 2], w.z, zp[o][2]);
-                        zp[o][3] = fmaf(h[j + 3], w.w, zp[o][3]);
+                        float zp[4] = {0.f, 0.f, 0.f, 0.f};
+                        for (int j = 0; j < 64; j += 4) {
+                            const float4 w = W2v[o * (H / 4) + j / 4];
+                            zp[0] = fmaf(h[j], w.x, zp[0]);
+                            zp[1] = fmaf(h[j + 1], w.y, zp[1]);
+                            zp[2] = fmaf(h[j + 2], w.z, zp[2]);
+                            zp[3] = fmaf(h[j + 3], w.w, zp[3]);
+                        }
+                        const float z = b2[o] + ((zp[0] + zp[1]) + (zp[2] + zp[3]));
+                        bad |= !isfinite(z) || hmax_bits >= 0x7f800000;
+                        s = fmaf(z, att[o], s);
                     }
                 }
-#pragma unroll
-                for (int o = 0; o < Z; ++o) {
-                    const float z = b2[o] + ((zp[o][0] + zp[o][1]) + (zp[o][2] + zp[o][3]));
-                    bad |= !isfinite(z);
-                    s = fmaf(z, att[o], s);
-                }
-                on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s, gi, my_s);
+                on_score(base + row, row < nv, bad ? __int_as_float(0x7fc00000) : s, gi, my_s, my_rank);
                 if (et) tmr[1] += clock64() - c0;
             }
             if (et) tmr[4] += clock64() - e_start;
