@@ -96,12 +96,20 @@ struct TcPipe2 {
                 const int grp = o >> 1, half = o & 1;
                 auto rows_of = [&](int t, int (&dst)[4]) {
                     const int base = t * TM, nv = t < T ? min(TM, n - base) : 0;
+                    int32_t sl[4];
+                    if (4 * grp + 3 < nv) {  // whole group: one 16-byte load (lists are 16-byte aligned)
+                        const int4 v = *reinterpret_cast<const int4 *>(slots + base + 4 * grp);
+                        sl[0] = v.x; sl[1] = v.y; sl[2] = v.z; sl[3] = v.w;
+                    } else {
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const int r = 4 * grp + j;
-                        const int32_t sl = r < nv ? slots[base + r] : -1;
-                        dst[j] = sl < 0 ? 0 : (it.hl_by_slot ? (int)sl : (int)slot_row(g, sl));
+                        for (int j = 0; j < 4; ++j) sl[j] = 4 * grp + j < nv ? slots[base + 4 * grp + j] : -1;
                     }
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        dst[j] = sl[j] < 0 ? 0 : (it.hl_by_slot ? (int)sl[j] : (int)slot_row(g, sl[j]));
+                    // the tile after: its slot ids into L2 now (the list may have left L2 since expand)
+                    if (t + 1 < T && (grp & 7) == 0 && half == 0)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(slots + base + TM + 4 * grp));
                 };
                 int nx[4];
                 rows_of(0, nx);
