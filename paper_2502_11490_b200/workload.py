@@ -168,24 +168,31 @@ def exact_graph(name: str, items, m: int, rank: int = 0) -> GraphIndex:
     key = hashlib.sha256(probe.tobytes()).hexdigest()[:16]
     cache = os.environ.get("GMPGR_CACHE", "/tmp/gmpgr_cache")
     path = os.path.join(cache, f"{name}_{N}x{d}_m{m}_ef64_{key}_v2.npz")
+    failed = path + ".failed"
     if not os.path.exists(path):
         if rank == 0:
             index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
             ids, levels, layers, entry = index.graph_view()
-            os.makedirs(cache, exist_ok=True)
-            arrs = {"ids": ids, "levels": levels, "entry": np.int64(entry), "m": np.int64(index.m),
-                    "max_layers": np.int64(index.max_layers)}
-            for l, (nb, ct) in enumerate(layers):  # upper layers: member rows only
-                rows = np.arange(N) if l == 0 else np.nonzero(levels[:N] >= l)[0]
-                arrs[f"rows{l}"], arrs[f"nb{l}"], arrs[f"ct{l}"] = rows, nb[rows], ct[rows]
-            tmp = path + f".tmp{os.getpid()}.npz"
-            np.savez(tmp, **arrs)
-            os.replace(tmp, path)
+            try:
+                os.makedirs(cache, exist_ok=True)
+                arrs = {"ids": ids, "levels": levels, "entry": np.int64(entry), "m": np.int64(index.m),
+                        "max_layers": np.int64(index.max_layers)}
+                for l, (nb, ct) in enumerate(layers):  # upper layers: member rows only
+                    rows = np.arange(N) if l == 0 else np.nonzero(levels[:N] >= l)[0]
+                    arrs[f"rows{l}"], arrs[f"nb{l}"], arrs[f"ct{l}"] = rows, nb[rows], ct[rows]
+                tmp = path + f".tmp{os.getpid()}.npz"
+                np.savez(tmp, **arrs)
+                os.replace(tmp, path)
+            except OSError:  # no room for the cache: the other ranks build their own copy
+                try:
+                    open(failed, "w").close()
+                except OSError:
+                    pass
             return index
         t0 = time.time()
         while not os.path.exists(path):
-            if time.time() - t0 > 3600:
-                raise TimeoutError(f"rank {rank}: no graph from rank 0 at {path}")
+            if os.path.exists(failed) or time.time() - t0 > 3600:
+                return GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
             time.sleep(2.0)
     z = np.load(path)
     nl = sum(1 for f in z.files if f.startswith("nb"))
