@@ -171,6 +171,8 @@ def exact_graph(name: str, items, m: int, rank: int = 0) -> GraphIndex:
     failed = path + ".failed"
     if not os.path.exists(path):
         if rank == 0:
+            if os.path.exists(failed):  # a marker left by an earlier run
+                os.remove(failed)
             index = GraphIndex.build(items.double().cpu().numpy(), m=m, ef_construction=64, seed=0)
             ids, levels, layers, entry = index.graph_view()
             try:
