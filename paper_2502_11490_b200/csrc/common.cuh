@@ -35,6 +35,24 @@ __device__ __forceinline__ void mac4(float4 &a, const float4 x, const float4 w) 
     a.z = __fadd_rn(__fmul_rn(x.z, w.z), a.z);
     a.w = __fadd_rn(__fmul_rn(x.w, w.w), a.w);
 }
+// mac4 in packed f32x2 instructions (FFMA2 + FADD2, half the issue slots): the product is
+// fma(x, w, nz) with nz = -0.0 passed at run time -- exactly fl(x * w) for every x, w (the
+// -0 addend changes neither a rounded product nor the sign of a zero one) -- and ptxas,
+// which does not know nz, cannot contract it with the add as it does mul.rn.f32x2 +
+// add.rn.f32x2.  Same per-lane arithmetic and order as mac4: a = fl(fl(x * w) + a).
+__device__ __forceinline__ void mac4x2(float4 &a, const float4 x, const float4 w, float nz) {
+    auto pk = [](float lo, float hi) {
+        return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+    };
+    const unsigned long long z2 = pk(nz, nz);
+    unsigned long long p0, p1, s0, s1;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p0) : "l"(pk(x.x, x.y)), "l"(pk(w.x, w.y)), "l"(z2));
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(p1) : "l"(pk(x.z, x.w)), "l"(pk(w.z, w.w)), "l"(z2));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s0) : "l"(p0), "l"(pk(a.x, a.y)));
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(s1) : "l"(p1), "l"(pk(a.z, a.w)));
+    a = make_float4(__uint_as_float((uint32_t)s0), __uint_as_float((uint32_t)(s0 >> 32)),
+                    __uint_as_float((uint32_t)s1), __uint_as_float((uint32_t)(s1 >> 32)));
+}
 __device__ __forceinline__ float hsum4(const float4 a) {
     return __fadd_rn(__fadd_rn(a.x, a.y), __fadd_rn(a.z, a.w));
 }

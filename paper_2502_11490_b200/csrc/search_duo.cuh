@@ -45,10 +45,12 @@ struct ExactU {
                          OFF_Z = EQ::OFF_Z, OFF_SC = EQ::OFF_SC, OFF_PQ = EQ::OFF_PQ,
                          BUF_END = EQ::BUF_END, W_END = EQ::W_END;
 
-    template <int NCH, int LDX, bool HAS_INIT>
+    // PK: packed f32x2 products (mac4x2; measured faster for the tensor-core mode's sparse
+    // re-scoring, slower for MODE 0's dense exact scoring, which keeps scalar mac4)
+    template <int NCH, int LDX, bool HAS_INIT, bool PK>
     static __device__ __forceinline__ void big(int lt, const float4 *__restrict__ X, const float4 *__restrict__ W,
                                                const float *__restrict__ bias, const float4 *__restrict__ acc0,
-                                               const int *__restrict__ pq, float *__restrict__ Y) {
+                                               const int *__restrict__ pq, float *__restrict__ Y, float nz) {
         const int warp = lt >> 5, lane = lt & 31;
         float4 a[4][2];
 #pragma unroll
@@ -70,8 +72,13 @@ struct ExactU {
 #pragma unroll
             for (int pp = 0; pp < 4; ++pp) {
                 const float4 x = xr[pp * LDX + j];
-                mac4(a[pp][0], x, w0);
-                mac4(a[pp][1], x, w1);
+                if constexpr (PK) {
+                    mac4x2(a[pp][0], x, w0, nz);
+                    mac4x2(a[pp][1], x, w1, nz);
+                } else {
+                    mac4(a[pp][0], x, w0);
+                    mac4(a[pp][1], x, w1);
+                }
             }
         }
         const float b0 = bias[lane], b1 = bias[lane + 32];
@@ -86,15 +93,15 @@ struct ExactU {
     }
 
     // W: weight block (ExactQ layout); buf: activation buffers; acc0: [G][64] float4
-    template <class Sync>
+    template <bool PK, class Sync>
     static __device__ __forceinline__ void tile(int lt, const float4 *W, float4 *buf, const float4 *acc0,
-                                                int n_valid, int *nonfinite, Sync sync) {
+                                                int n_valid, int *nonfinite, Sync sync, float nz) {
         const int *pq = reinterpret_cast<const int *>(buf + OFF_PQ);
-        big<NCH0, LDX0, true>(lt, buf + OFF_X0, W + EQ::OFF_W0, reinterpret_cast<const float *>(W + EQ::OFF_B0),
-                              acc0, pq, reinterpret_cast<float *>(buf + OFF_H0));
+        big<NCH0, LDX0, true, PK>(lt, buf + OFF_X0, W + EQ::OFF_W0, reinterpret_cast<const float *>(W + EQ::OFF_B0),
+                              acc0, pq, reinterpret_cast<float *>(buf + OFF_H0), nz);
         sync();
-        big<NCHH, LDH, false>(lt, buf + OFF_H0, W + EQ::OFF_W1, reinterpret_cast<const float *>(W + EQ::OFF_B1),
-                              nullptr, pq, reinterpret_cast<float *>(buf + OFF_H1));
+        big<NCHH, LDH, false, PK>(lt, buf + OFF_H0, W + EQ::OFF_W1, reinterpret_cast<const float *>(W + EQ::OFF_B1),
+                              nullptr, pq, reinterpret_cast<float *>(buf + OFF_H1), nz);
         sync();
         float *zb = reinterpret_cast<float *>(buf + OFF_Z);
         if (lt < PT * Z) {
@@ -366,7 +373,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         if (lane == 0) pq[p] = p < nv ? (fr_i[base + p] >> 16) : 0;
                     }
                     usync();
-                    EX::tile(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync);
+                    EX::template tile<false>(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync, a.negz);
                     if (lt < 32) {
                         const bool valid = lt < nv;
                         const int32_t es = valid ? fr_v[base + lt] : 0;
@@ -402,7 +409,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         }
                     }
                     usync();
-                    EX::tile(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync);
+                    EX::template tile<true>(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync, a.negz);
                     if (lt < nv) {
                         const int e = rq[base + lt];
                         const int gq = e >> 24, idx = e & 0xFFFFFF;

@@ -87,6 +87,7 @@ struct SearchArgs {
     int *qdone;
     int chunk_q;
     int exp;  // GMPGR_EXP: timing experiments only (results not exact when set)
+    float negz;  // -0.0f: the run-time addend of the packed exact products (common.cuh mac4x2)
 };
 
 // Tensor-core mode certificate (run time).  The refinement argument (see below) needs
