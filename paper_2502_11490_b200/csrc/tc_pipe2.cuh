@@ -238,8 +238,10 @@ struct TcPipe2 {
 #pragma unroll
                     for (int j = 0; j < 16; j += 4) {
                         const float4 uo = *reinterpret_cast<const float4 *>(uq + o + j);
-                        const float y0 = fmaxf(h[o + j] + uo.x, 0.f), y1 = fmaxf(h[o + j + 1] + uo.y, 0.f);
-                        const float y2 = fmaxf(h[o + j + 2] + uo.z, 0.f), y3 = fmaxf(h[o + j + 3] + uo.w, 0.f);
+                        float y0, y1, y2, y3;
+                        tc::add2(y0, y1, h[o + j], h[o + j + 1], uo.x, uo.y);
+                        tc::add2(y2, y3, h[o + j + 2], h[o + j + 3], uo.z, uo.w);
+                        y0 = fmaxf(y0, 0.f); y1 = fmaxf(y1, 0.f); y2 = fmaxf(y2, 0.f); y3 = fmaxf(y3, 0.f);
                         uint2 hh, ll;
                         tc::split4(make_float4(y0, y1, y2, y3), hh, ll);
                         hi[j / 2] = hh.x; hi[j / 2 + 1] = hh.y;
@@ -262,10 +264,12 @@ struct TcPipe2 {
                     // relu output (negative values have the sign bit set) and catches NaN / +inf
                     int hbits = 0;
 #pragma unroll
-                    for (int j = 0; j < 64; ++j) {
-                        const float x = h[j] + b1[j];
-                        hbits = max(hbits, __float_as_int(x));
-                        h[j] = fmaxf(x, 0.f);
+                    for (int j = 0; j < 64; j += 2) {
+                        float x0, x1;
+                        tc::add2(x0, x1, h[j], h[j + 1], b1[j], b1[j + 1]);
+                        hbits = max(hbits, max(__float_as_int(x0), __float_as_int(x1)));
+                        h[j] = fmaxf(x0, 0.f);
+                        h[j + 1] = fmaxf(x1, 0.f);
                     }
                     hmax_bits = hbits;
                 }
@@ -284,10 +288,8 @@ struct TcPipe2 {
 #pragma unroll
                     for (int j = 0; j < 64; j += 4) {
                         const float4 w = wv[j / 4];
-                        sp[0] = fmaf(h[j], w.x, sp[0]);
-                        sp[1] = fmaf(h[j + 1], w.y, sp[1]);
-                        sp[2] = fmaf(h[j + 2], w.z, sp[2]);
-                        sp[3] = fmaf(h[j + 3], w.w, sp[3]);
+                        tc::fma2(sp[0], sp[1], h[j], h[j + 1], w.x, w.y);
+                        tc::fma2(sp[2], sp[3], h[j + 2], h[j + 3], w.z, w.w);
                     }
                     s = weff[64] + ((sp[0] + sp[1]) + (sp[2] + sp[3]));
                 } else {

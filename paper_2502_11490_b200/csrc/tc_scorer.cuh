@@ -217,6 +217,22 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float a, float b) {
     return *reinterpret_cast<const uint32_t *>(&h);
 }
 
+// packed f32x2 helpers for the approximate epilogue (any rounding order is fine there)
+__device__ __forceinline__ unsigned long long f2pk(float lo, float hi) {
+    return ((unsigned long long)__float_as_uint(hi) << 32) | __float_as_uint(lo);
+}
+__device__ __forceinline__ void add2(float &r0, float &r1, float a0, float a1, float b0, float b1) {
+    unsigned long long r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(f2pk(a0, a1)), "l"(f2pk(b0, b1)));
+    r0 = __uint_as_float((uint32_t)r);
+    r1 = __uint_as_float((uint32_t)(r >> 32));
+}
+__device__ __forceinline__ void fma2(float &c0, float &c1, float a0, float a1, float b0, float b1) {
+    unsigned long long r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(f2pk(a0, a1)), "l"(f2pk(b0, b1)), "l"(f2pk(c0, c1)));
+    c0 = __uint_as_float((uint32_t)r);
+    c1 = __uint_as_float((uint32_t)(r >> 32));
+}
 // split 4 fp32 into bf16 hi/lo pairs packed as 2 x u32 each
 __device__ __forceinline__ void split4(float4 x, uint2 &hi, uint2 &lo) {
     // hi = bf16(x), lo = bf16(x - hi); cvt.rn.bf16x2.f32 packs two lanes per instruction
