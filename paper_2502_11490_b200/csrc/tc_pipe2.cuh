@@ -124,7 +124,9 @@ struct TcPipe2 {
                         if (r >= 1) {
                             const long long c0 = clk();
                             // suspended, not spinning: the epilogue warps share these SMSPs
-                            tc::mbar_wait_hint(bar(u, EMPTY0 + s), (r - 1) & 1u, 2000u);
+                            // poll with a back-off: the loaders' spinning would take issue slots
+                            // from the epilogue warps on the same SMSPs
+                            while (!tc::mbar_test(bar(u, EMPTY0 + s), (r - 1) & 1u)) __nanosleep(64);
                             if (timed && lw == 0) tmr[7] += clk() - c0;
                         }
                         if ((exp & 1) && half) {  // experiment: hi rows only
