@@ -442,6 +442,8 @@ def run_gmpgr(args):
                     evals=st[:, 0], rows=st[:, 3], nbrs=st[:, 4], clocks=clk.summary() if clocks else None,
                     ids=out_ids.cpu().numpy(), scores=out_sc.cpu().numpy())
 
+    T0 = time.perf_counter()
+    log(f"[rank {rank}] timed search")
     main_m = measure(dict(PARAMS), args.steps, args.warmup, clocks=True)
     elapsed, per_launch = main_m["elapsed"], main_m["per_launch"]
     total_q = Q * args.steps * world
@@ -488,6 +490,7 @@ def run_gmpgr(args):
                                        "(numpy einsum order); in tc mode only the re-scored "
                                        "band runs on CUDA cores"}}
 
+    log(f"[rank {rank}] e2e ({time.perf_counter() - T0:.0f}s)")
     # ---- e2e through the public API with host buffers (H2D users, D2H results)
     pin_users = torch.from_numpy(wl.users).pin_memory()
     h_ids = torch.empty((Q, k), dtype=torch.int64).pin_memory()
@@ -516,6 +519,7 @@ def run_gmpgr(args):
     d2h = Q * k * 16 + Q * 4 + Q * (5 + L) * 8
     assert np.array_equal(h_ids.numpy(), dev_ids), "host-API results differ from the device-timed run"
 
+    log(f"[rank {rank}] recall ({time.perf_counter() - T0:.0f}s)")
     # ---- recall@100 vs exact brute force (GPU, all items) on a query subset
     nrec = min(Q, args.recall_queries)
     gt_ids, _ = brute_force_batch(metric, wl.users[:nrec], wl.items, 100, device=dev)
@@ -570,6 +574,7 @@ def run_gmpgr(args):
                 [len(set(dev_ids[q]) & set(gold["gt100"][q])) / 100.0 for q in range(ng)]))
             rp["reference_recall_at_100"] = float(gold[f"p{pi}/recall100"])
         line["reference_parity"] = rp
+    log(f"[rank {rank}] operating points ({time.perf_counter() - T0:.0f}s)")
     # ---- further operating points of the same workload (higher recall budgets)
     if args.operating_points and rank == 0 or (args.operating_points and dist):
         ops = []
@@ -590,6 +595,7 @@ def run_gmpgr(args):
                                                       m["scores"][:nq], m["evals"][:nq])
             ops.append(op)
         line["operating_points"] = ops
+    log(f"[rank {rank}] own graph ({time.perf_counter() - T0:.0f}s)")
     line["resident_units"] = searcher.counters().get("resident_units")
     # ---- the same queries on this repo's own bulk GPU graph producer (builder.py): a second
     # graph of the same items (the exact-graph line above is the reference-faithful headline)
@@ -615,6 +621,7 @@ def run_gmpgr(args):
                                   "roofline_frac": b / m["per_launch"] / 1e9 / pk["hbm_gbs"]})
         line["own_graph"] = own
         del g2, gidx
+    log(f"[rank {rank}] cpu baseline + stock reference ({time.perf_counter() - T0:.0f}s)")
     if want_cpu and rank == 0:
         r, n, t, threads = cpu_baseline(wl, target_s=args.cpu_s)
         line["cpu_baseline"] = {"value": n / t, "unit": "queries/s", "cores": threads,
