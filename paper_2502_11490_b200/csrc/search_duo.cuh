@@ -262,8 +262,9 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     // ---- scratch: unit-level flattened lists, per-query visited bitsets / logs / pools
     const int64_t ug = (int64_t)blockIdx.x * 2 + unit;  // global unit index
     const int64_t capF = a.capF, capS = a.capS, capP = a.capP;  // lists already x G
-    int32_t *fslot[2] = {a.f_slot + ug * 2 * capF, a.f_slot + ug * 2 * capF + capF};
-    int32_t *fsrch[2] = {a.f_srch + ug * 2 * capF, a.f_srch + ug * 2 * capF + capF};
+    // frontier lists c = 0/1 (pointer arithmetic, not a dynamically indexed local array)
+    auto fslot = [&](int c) { return a.f_slot + (ug * 2 + c) * capF; };
+    auto fsrch = [&](int c) { return a.f_srch + (ug * 2 + c) * capF; };
     int32_t *surv_v = a.surv_v + ug * capS, *surv_i = a.surv_i + ug * capS;
     int32_t *cont_v = a.cont_v + ug * capS, *cont_i = a.cont_i + ug * capS;
     // fresh claims ARE the survivors (unique per (query, node)); their searcher field is
@@ -587,8 +588,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             for (int gq = 0; gq < G; ++gq) {
                 const MqQuery &Q = st.qs[gq];
                 for (int i = lt; i < Q.f_cnt; i += NTH) {
-                    fslot[0][Q.f_off + i] = pslot(gq, Q.pool_cur)[sortv[gq * a.sortcap + i]];
-                    fsrch[0][Q.f_off + i] = (gq << 16) | i;
+                    fslot(0)[Q.f_off + i] = pslot(gq, Q.pool_cur)[sortv[gq * a.sortcap + i]];
+                    fsrch(0)[Q.f_off + i] = (gq << 16) | i;
                 }
             }
             usync();
@@ -622,8 +623,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         wg = -1;
                         if (base + lane < qend) {
                             GR_DCHECK(base + lane < capF, "fslot index %d >= %lld", base + lane, (long long)capF);
-                            ws = fslot[fc][base + lane];
-                            wg = fsrch[fc][base + lane];
+                            ws = fslot(fc)[base + lane];
+                            wg = fsrch(fc)[base + lane];
                             if (layer == 0) {  // rows of the next batches: L2 ahead of the piece loads
                                 const char *rp = reinterpret_cast<const char *>(g.adj[0] + (int64_t)ws * g.ld[0]);
                                 for (int o = 0; o < g.ld[0] * 4; o += 128)
@@ -819,7 +820,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                     const int gi = ((sg / a.kp) << 16) | (sg % a.kp);
                     if (ni <= a.ef) {
                         GR_DCHECK(fo + ni <= capF, "frontier write %d + %d > %lld", fo, ni, (long long)capF);
-                        for (int j = lane; j < ni; j += 32) { fslot[fn][fo + j] = seg_v[off + j]; fsrch[fn][fo + j] = gi; }
+                        for (int j = lane; j < ni; j += 32) { fslot(fn)[fo + j] = seg_v[off + j]; fsrch(fn)[fo + j] = gi; }
                     } else {
                         const uint64_t T = warp_select_threshold(seg_key + off, ni, a.ef, hist + warp * 256);
                         int cnt = 0;
@@ -829,8 +830,8 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                             const unsigned mask = __ballot_sync(0xffffffffu, keep);
                             if (keep) {
                                 const int pos = fo + cnt + __popc(mask & ((1u << lane) - 1u));
-                                fslot[fn][pos] = seg_v[off + j];
-                                fsrch[fn][pos] = gi;
+                                fslot(fn)[pos] = seg_v[off + j];
+                                fsrch(fn)[pos] = gi;
                             }
                             cnt += __popc(mask);
                         }

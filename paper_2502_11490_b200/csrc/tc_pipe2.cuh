@@ -82,7 +82,12 @@ struct TcPipe2 {
         // [2] D0FULL wait, [3] D1FULL wait, [4] epilogue total, [5] issuer idle polls,
         // [6] issuer issuing, [7] loader EMPTY wait (cycles of one thread per role)
         const int warp = lt >> 5, lane = lt & 31;
+#ifdef GMPGR_PIPE_TIMERS
         const bool timed = tmr && lane == 0;
+#else
+        constexpr bool timed = false;  // role timers compiled out (registers): -DGMPGR_PIPE_TIMERS
+        (void)tmr;
+#endif
         auto clk = [&]() { return timed ? clock64() : 0ll; };
         const int T = (n + TM - 1) / TM;
         if (T == 0) return;
@@ -212,7 +217,7 @@ struct TcPipe2 {
             // ================= epilogue: row = TMEM lane
             const int q4 = warp & 3, row = q4 * 32 + lane;
             const uint32_t lanebase = (uint32_t)(q4 * 32) << 16;
-            const bool et = timed && warp == 0;
+            const bool et = timed && warp == 0;  // folds to false unless GMPGR_PIPE_TIMERS
             const long long e_start = et ? clock64() : 0;
             for (int t = 0; t < T; ++t) {
                 const uint32_t tg = tile_ctr + t;
