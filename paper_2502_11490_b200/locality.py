@@ -15,10 +15,15 @@ from __future__ import annotations
 import numpy as np
 
 
-def cluster_order(emb, slot_rows=None, per_cluster: int = 2048, iters: int = 5, seed: int = 0,
+def cluster_order(emb, slot_rows=None, per_cluster: int | None = None, iters: int = 5, seed: int = 0,
                   device: int = 0) -> np.ndarray:
     """int64 permutation: caller slots grouped by k-means cluster of their embedding row."""
+    import os
+
     import torch
+
+    if per_cluster is None:
+        per_cluster = int(os.environ.get("GMPGR_CLUSTER", "2048"))
 
     dev = torch.device("cuda", device)
     x = emb if isinstance(emb, torch.Tensor) else torch.from_numpy(np.ascontiguousarray(emb))
@@ -48,5 +53,19 @@ def cluster_order(emb, slot_rows=None, per_cluster: int = 2048, iters: int = 5, 
         cnt = torch.bincount(a, minlength=K).to(sums.dtype)[:, None]
         cent = torch.where(cnt > 0, sums / cnt.clamp_min(1.0), cent)
     lab = assign(x, cent)
+    import os
+
+    if K >= 16 and os.environ.get("GMPGR_ORDER2", "0") != "0":
+        # second level: clusters grouped by a k-means of their centroids (~sqrt(K) groups),
+        # so clusters that share graph edges also sit near each other in slot space
+        K2 = max(2, int(round(K ** 0.5)))
+        c2 = cent[torch.randperm(K, generator=g, device=dev)[:K2]].clone()
+        for _ in range(iters):
+            a2 = assign(cent, c2)
+            s2 = torch.zeros_like(c2).index_add_(0, a2, cent)
+            n2 = torch.bincount(a2, minlength=K2).to(s2.dtype)[:, None]
+            c2 = torch.where(n2 > 0, s2 / n2.clamp_min(1.0), c2)
+        sup = assign(cent, c2)
+        lab = sup[lab] * K + lab
     order = torch.sort(lab, stable=True).indices
     return order.cpu().numpy().astype(np.int64)
