@@ -280,3 +280,27 @@ def test_tensor_core_mode_large_batch_matches_reference(P, fixture):
         np.testing.assert_array_equal(r.scores[sl], exp["scores"])
         np.testing.assert_array_equal(r.evals[sl], exp["evals"])
         np.testing.assert_array_equal(r.hops_to_best[sl], exp["best_hop"])
+
+
+def test_tensor_core_head_overflow_guard_path(P):
+    """Head weights scaled so the epilogue's largest relu output often exceeds its no-overflow
+    limit: those rows take the per-head path (non-finite check per head) instead of the
+    collapsed dot product -- results still equal exact mode, and nothing is flagged."""
+    rng = np.random.default_rng(13)
+    n, d = 20_000, 128
+    model = P.create_model(d_x=d, d_h=d, z_dim=3, hidden=(64, 64), seed=1)
+    w2, b2 = model.metric.layers[-1]
+    w2 *= np.float32(1e35)  # |z| ~ 1e36: finite, but h_max above the guard's limit (~15)
+    centers = rng.normal(scale=4.0, size=(128, d))
+    feats = (centers[rng.integers(0, 128, size=n)] + rng.normal(size=(n, d))).astype(np.float32)
+    emb = model.item_embeddings(feats).astype(np.float32)
+    index = P.GraphIndex.build(emb, m=16, seed=0)
+    users = model.user_embedding(rng.normal(size=(64, d)).astype(np.float32)).astype(np.float32)
+    kw = dict(k=100, k_parallel=8, hops=3, ef=200)
+    ex = P.c_hipanns_batch(index, model, users, emb, P.SearchParams(**kw))
+    tc = P.c_hipanns_batch(index, model, users, emb, P.SearchParams(**kw, mode="tc"))
+    assert np.all(np.isfinite(ex.scores[ex.ids >= 0]))
+    assert np.abs(ex.scores[ex.ids >= 0]).max() > 1e30
+    np.testing.assert_array_equal(tc.ids, ex.ids)
+    np.testing.assert_array_equal(tc.scores, ex.scores)
+    np.testing.assert_array_equal(tc.evals, ex.evals)
