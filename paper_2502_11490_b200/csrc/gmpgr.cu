@@ -1225,7 +1225,6 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     a.avail = avail;
     a.qdone = qdone;
     a.chunk_q = chunk_q;
-    if (const char *e = getenv("GMPGR_EXP")) a.exp = atoi(e);
     a.negz = -0.0f;
     GR_CUDA(cudaMemsetAsync(S->flags, 0, sizeof(int), stream));
     kern<<<(int)(units / 2), 512, smem, stream>>>(a);

@@ -353,7 +353,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
             if constexpr (MODE == 1) {
                 TP::run(smem, ub, U, sb1, sW2, sb2, satt, tmem, a.it, g, fr_v, fr_i, n, chunk_ctr, tile_ctr, lt,
                         on_score, usync, &a.hl_map,
-                        a.phase_cycles && unit == 0 ? ph_acc + 8 : nullptr, a.exp);
+                        a.phase_cycles && unit == 0 ? ph_acc + 8 : nullptr);
                 if (lt == 0) atomicAdd(a.counters + 1, (unsigned long long)n);
             } else {
                 int *pq = reinterpret_cast<int *>(sBuf + EX::OFF_PQ);

@@ -86,7 +86,6 @@ struct SearchArgs {
     const int *avail;
     int *qdone;
     int chunk_q;
-    int exp;  // GMPGR_EXP: timing experiments only (results not exact when set)
     float negz;  // -0.0f: the run-time addend of the packed exact products (common.cuh mac4x2)
 };
 

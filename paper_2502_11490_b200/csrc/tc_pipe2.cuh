@@ -77,7 +77,7 @@ struct TcPipe2 {
                                                const DevGraph &g, const int32_t *slots, const int32_t *gis,
                                                int n, uint32_t &chunk_ctr, uint32_t &tile_ctr, int lt,
                                                OnScore on_score, Sync sync, const void *tmap,
-                                               unsigned long long *tmr = nullptr, int exp = 0) {
+                                               unsigned long long *tmr = nullptr) {
         // tmr (GMPGR_PHASE_TIMING, unit 0): [0] epilogue layer-0 work, [1] layer-1 work,
         // [2] D0FULL wait, [3] D1FULL wait, [4] epilogue total, [5] issuer idle polls,
         // [6] issuer issuing, [7] loader EMPTY wait (cycles of one thread per role)
@@ -133,10 +133,6 @@ struct TcPipe2 {
                             // from the epilogue warps on the same SMSPs
                             while (!tc::mbar_test(bar(u, EMPTY0 + s), (r - 1) & 1u)) __nanosleep(64);
                             if (timed && lw == 0) tmr[7] += clk() - c0;
-                        }
-                        if ((exp & 1) && half) {  // experiment: hi rows only
-                            tc::mbar_arrive(bar(u, FULL0 + s));
-                            continue;
                         }
                         tc::mbar_arrive_expect_tx(bar(u, FULL0 + s), 512);
                         tc::tma_gather4(tc::smem_u32(u + OFF_A + s * 2 * CH_BYTES) + half * CH_BYTES + grp * 512,
@@ -194,10 +190,8 @@ struct TcPipe2 {
                             const uint32_t kb = (l0k * (KC / 16) + k) * 256;
                             const uint64_t bh = tc::desc(bH0 + kb, D_H), bl = tc::desc(bL0 + kb, D_H);
                             tc::mma_w(d0, ah, bh, IDESC, (l0k | k) ? 1u : 0u);  // hi . W_hi
-                            if (!(exp & 2)) {  // experiment 2: hi . W_hi only
-                                tc::mma_w(d0, ah, bl, IDESC, 1u);                // hi . W_lo
-                                tc::mma_w(d0, al, bh, IDESC, 1u);                // lo . W_hi
-                            }
+                            tc::mma_w(d0, ah, bl, IDESC, 1u);                // hi . W_lo
+                            tc::mma_w(d0, al, bh, IDESC, 1u);                // lo . W_hi
                         }
                         tc::commit_w(bar(u, EMPTY0 + s));
                         if (++l0k == NC) {
