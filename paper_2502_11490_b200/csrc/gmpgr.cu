@@ -198,10 +198,11 @@ struct gr_searcher {
                 *seg_v = nullptr, *pool_slot = nullptr, *pool_meta = nullptr, *vlog = nullptr;
         uint64_t *fr_key = nullptr, *seg_key = nullptr, *pool_key = nullptr, *hash = nullptr;
         uint32_t *vis = nullptr;
+        float4 *acc0 = nullptr;  // [units][G][64] hoisted user halves (tensor-core mode)
         size_t bytes = 0;
         void free_all() {
             void *ps[] = {f_slot, f_srch, surv_v, surv_i, cont_v, cont_i, fr_v, fr_i, seg_v, pool_slot,
-                          pool_meta, vlog, fr_key, seg_key, pool_key, hash, vis};
+                          pool_meta, vlog, fr_key, seg_key, pool_key, hash, vis, acc0};
             for (void *p : ps)
                 if (p) cudaFree(p);
             *this = Duo();
@@ -1024,7 +1025,7 @@ size_t duo_unit_bytes(int64_t G, int64_t capF, int64_t capS, int64_t capP, int64
                       int64_t logcap) {
     const int64_t lF = capF * G, lS = capS * G;
     return (size_t)(2 * 2 * lF * 4 + 5 * lS * 4 + 2 * lS * 8 + hcap * 8 + G * 2 * capP * 16 + G * vwords * 4 +
-                    G * logcap * 4);
+                    G * logcap * 4 + G * 64 * 16);
 }
 
 int ensure_duo_scratch(gr_searcher *S, int64_t units, int64_t G, int64_t capF, int64_t capS, int64_t capP,
@@ -1049,6 +1050,7 @@ int ensure_duo_scratch(gr_searcher *S, int64_t units, int64_t G, int64_t capF, i
     if ((rc = dmalloc(&D.pool_meta, (size_t)slots * 2 * capP))) return rc;
     if ((rc = dmalloc(&D.vis, (size_t)slots * vwords))) return rc;
     if ((rc = dmalloc(&D.vlog, (size_t)slots * logcap))) return rc;
+    if ((rc = dmalloc(&D.acc0, (size_t)slots * 64))) return rc;
     if (hcap) GR_CUDA(cudaMemset(D.hash, 0xFF, (size_t)units * hcap * 8));
     GR_CUDA(cudaMemset(D.vis, 0, (size_t)slots * vwords * 4));
     D.units = units;
@@ -1069,8 +1071,12 @@ int plan_duo(int k, int kp, SearchArgs &a) {
     using TP = TcPipe2<DH, ZZ>;
     a.sortcap = pow2ceil(std::max(k, kp));
     const int hist_b = 8 * 256 * 4, sortk_b = G * a.sortcap * 8, sortv_b = G * a.sortcap * 4;
-    const int shared_b = MODE == 1 ? TP::B_BYTES : EX::W_END * 16;
+    int shared_b = MODE == 1 ? TP::B_BYTES : EX::W_END * 16;
     auto up = [](int x, int al) { return (x + al - 1) / al * al; };
+    if (MODE == 1) {  // + the exact re-scorer's layer-0 weights (item half)
+        a.off_exw0 = up(shared_b, 16);
+        shared_b = a.off_exw0 + EX::NCH0 * 64 * 16;
+    }
     a.unit0 = up(shared_b, 1024);
     SmemPlan U;  // unit-relative
     int alias_end = 0;
@@ -1094,7 +1100,7 @@ int plan_duo(int k, int kp, SearchArgs &a) {
     a.off_sortk = place(sortk_b);
     a.off_sortv = place(sortv_b);
     a.off_misc = U.alloc((G * 64 + 64 + 64 * ZZ + 8 + 64 + 4) * 4);  // + w_eff, c0, hlim
-    a.off_acc0 = U.alloc(G * 64 * 16);
+    if (MODE == 0) a.off_acc0 = U.alloc(G * 64 * 16);  // MODE 1: global (SearchArgs::acc0g)
     a.off_kp = U.alloc(3 * G * kp * 4);
     a.unit_stride = up(U.bytes, 1024);
     a.off_tmemp = a.unit0 + 2 * a.unit_stride;
@@ -1211,6 +1217,7 @@ int launch_duo(gr_searcher *S, const gr_graph *G, const gr_model *M, const gr_it
     a.vis = D.vis;
     a.vis_words = D.vwords;
     a.vlog = D.vlog;
+    a.acc0g = D.acc0;
     a.log_cap = (int)D.logcap;
     a.counters = S->counters;
     a.phase_cycles = S->phase;

@@ -94,10 +94,11 @@ struct ExactU {
 
     // W: weight block (ExactQ layout); buf: activation buffers; acc0: [G][64] float4
     template <bool PK, class Sync>
-    static __device__ __forceinline__ void tile(int lt, const float4 *W, float4 *buf, const float4 *acc0,
-                                                int n_valid, int *nonfinite, Sync sync, float nz) {
+    static __device__ __forceinline__ void tile(int lt, const float4 *W, const float4 *W0, float4 *buf,
+                                                const float4 *acc0, int n_valid, int *nonfinite, Sync sync,
+                                                float nz) {
         const int *pq = reinterpret_cast<const int *>(buf + OFF_PQ);
-        big<NCH0, LDX0, true, PK>(lt, buf + OFF_X0, W + EQ::OFF_W0, reinterpret_cast<const float *>(W + EQ::OFF_B0),
+        big<NCH0, LDX0, true, PK>(lt, buf + OFF_X0, W0, reinterpret_cast<const float *>(W + EQ::OFF_B0),
                               acc0, pq, reinterpret_cast<float *>(buf + OFF_H0), nz);
         sync();
         big<NCHH, LDH, false, PK>(lt, buf + OFF_H0, W + EQ::OFF_W1, reinterpret_cast<const float *>(W + EQ::OFF_B1),
@@ -197,6 +198,11 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
         const uint4 *src = reinterpret_cast<const uint4 *>(M.tcB);
         uint4 *dst = reinterpret_cast<uint4 *>(smem + TP::OFF_B0H);
         for (int t = tid; t < TP::B_BYTES / 16; t += 512) dst[t] = src[t];
+        // the exact re-scorer's layer-0 weights (item half, the bulk of its MACs) in shared
+        // memory too: the rest of its block is read through L1 from M.exBlock
+        const float4 *w0s = reinterpret_cast<const float4 *>(M.exBlock) + EX::EQ::OFF_W0;
+        float4 *w0d = reinterpret_cast<float4 *>(smem + a.off_exw0);
+        for (int t = tid; t < EX::NCH0 * 64; t += 512) w0d[t] = w0s[t];
     } else {
         const float4 *src = reinterpret_cast<const float4 *>(M.exBlock);
         float4 *dst = reinterpret_cast<float4 *>(smem);
@@ -205,7 +211,11 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
     unsigned char *const ub = smem + a.unit0 + unit * a.unit_stride;  // this unit's block
     const float4 *sW = MODE == 1 ? reinterpret_cast<const float4 *>(M.exBlock) : reinterpret_cast<const float4 *>(smem);
     float4 *sBuf = reinterpret_cast<float4 *>(ub + a.off_x0);
-    float4 *sAcc0 = reinterpret_cast<float4 *>(ub + a.off_acc0);
+    // hoisted user halves: shared memory in MODE 0, global (per unit) in MODE 1
+    float4 *sAcc0 = MODE == 1 ? a.acc0g + ((int64_t)blockIdx.x * 2 + unit) * G * 64
+                              : reinterpret_cast<float4 *>(ub + a.off_acc0);
+    const float4 *sW0 = MODE == 1 ? reinterpret_cast<const float4 *>(smem + a.off_exw0)
+                                  : reinterpret_cast<const float4 *>(smem) + EX::EQ::OFF_W0;
     uint32_t *hist = reinterpret_cast<uint32_t *>(ub + a.off_hist);
     uint64_t *sortk = reinterpret_cast<uint64_t *>(ub + a.off_sortk);
     int32_t *sortv = reinterpret_cast<int32_t *>(ub + a.off_sortv);
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         if (lane == 0) pq[p] = p < nv ? (fr_i[base + p] >> 16) : 0;
                     }
                     usync();
-                    EX::template tile<false>(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync, a.negz);
+                    EX::template tile<false>(lt, sW, sW0, sBuf, sAcc0, nv, a.nonfinite, usync, a.negz);
                     if (lt < 32) {
                         const bool valid = lt < nv;
                         const int32_t es = valid ? fr_v[base + lt] : 0;
@@ -410,7 +420,7 @@ __global__ void __launch_bounds__(512, 1) hipanns_duo_kernel(const __grid_consta
                         }
                     }
                     usync();
-                    EX::template tile<true>(lt, sW, sBuf, sAcc0, nv, a.nonfinite, usync, a.negz);
+                    EX::template tile<true>(lt, sW, sW0, sBuf, sAcc0, nv, a.nonfinite, usync, a.negz);
                     if (lt < nv) {
                         const int e = rq[base + lt];
                         const int gq = e >> 24, idx = e & 0xFFFFFF;

@@ -87,6 +87,8 @@ struct SearchArgs {
     int *qdone;
     int chunk_q;
     float negz;  // -0.0f: the run-time addend of the packed exact products (common.cuh mac4x2)
+    int off_exw0;       // duo MODE 1: shared-memory copy of the exact layer-0 (item half) weights
+    float4 *acc0g;      // duo MODE 1: [units][G][64] hoisted user halves (global; MODE 0 keeps them in smem)
 };
 
 // Tensor-core mode certificate (run time).  The refinement argument (see below) needs
